@@ -1,0 +1,67 @@
+// hooks.hpp — the user hook contract, device side.
+//
+// A model is a trivially copyable struct with compile-time widths and the
+// reference's hook names and std::span signatures
+// (/root/reference/proj/include/odensemble/system.hpp:49-65):
+//
+//   ode_rhs            <- paper: OdeFunction
+//   event_values       <- paper: EventFunction
+//   event_action       <- paper: ActionAfterEventDetection
+//   event_accessory    <- paper: EventAccessories
+//   ordinary_accessory <- paper: ActionAfterSuccessfulTimeStep / OrdinaryAccessories
+//   initialize         <- paper: Initialization
+//   finalize           <- paper: Finalization
+//
+// The struct is copied by value into the kernel's parameter bank, so hook
+// data (e.g. a ramp slope) costs no registers until used; the hooks are
+// inlined into the per-thread step loop (never called through pointers).
+// Host-only parts (ode_controls(), event_controls()) live in the System
+// classes of the C++ host API (include/odegpu/system.hpp).
+#ifndef ODEGPU_HOOKS_HPP
+#define ODEGPU_HOOKS_HPP
+
+#include <concepts>
+#include <span>
+#include <type_traits>
+
+#include "odegpu/core.hpp"
+
+namespace odegpu {
+
+/// No-op implementations of every optional hook (system.hpp:70-78).
+struct HookDefaults {
+    ODEGPU_HD void event_values(Real, std::span<const Real>, std::span<const Real>, std::span<Real>) const {}
+    ODEGPU_HD void event_action(Index, Index, Real, std::span<Real>, std::span<const Real>) const {}
+    ODEGPU_HD void ordinary_accessory(Real, std::span<const Real>, std::span<const Real>, std::span<Real>) const {}
+    ODEGPU_HD void event_accessory(Index, Index, Real, std::span<const Real>, std::span<const Real>,
+                                   std::span<Real>) const {}
+    ODEGPU_HD void initialize(Real, std::span<Real>, std::span<Real>, std::span<const Real>, std::span<Real>) const {}
+    ODEGPU_HD void finalize(Real, std::span<Real>, std::span<Real>, std::span<const Real>, std::span<Real>) const {}
+};
+
+// clang-format off
+/// Device-side half of the reference's SystemModel concept (system.hpp:49-65):
+/// the hooks plus compile-time widths so per-thread state can live in
+/// registers.
+template <typename H>
+concept DeviceHooks = std::is_trivially_copyable_v<H> &&
+    requires(const H& d, Real t, std::span<const Real> y, std::span<const Real> p,
+             std::span<Real> out, std::span<Real> my, std::span<Real> td, std::span<Real> acc,
+             Index ei, Index ec) {
+    { H::kSystemDim } -> std::convertible_to<Index>;
+    { H::kParamCount } -> std::convertible_to<Index>;
+    { H::kEventCount } -> std::convertible_to<Index>;
+    { H::kAccessoryCount } -> std::convertible_to<Index>;
+    { d.ode_rhs(t, y, p, out) } -> std::same_as<void>;
+    { d.event_values(t, y, p, out) } -> std::same_as<void>;
+    { d.event_action(ei, ec, t, my, p) } -> std::same_as<void>;
+    { d.ordinary_accessory(t, y, p, acc) } -> std::same_as<void>;
+    { d.event_accessory(ei, ec, t, y, p, acc) } -> std::same_as<void>;
+    { d.initialize(t, td, my, p, acc) } -> std::same_as<void>;
+    { d.finalize(t, td, my, p, acc) } -> std::same_as<void>;
+};
+// clang-format on
+
+} // namespace odegpu
+
+#endif

@@ -1,0 +1,126 @@
+// Duffing oscillator models, hook side (device + host).
+// Restates /root/reference/proj/include/odensemble/models/duffing.hpp.
+#ifndef ODEGPU_MODELS_DUFFING_HPP
+#define ODEGPU_MODELS_DUFFING_HPP
+
+#include <cmath>
+#include <span>
+
+#include "odegpu/hooks.hpp"
+
+namespace odegpu::models {
+
+/// y1' = y2, y2' = delta*y1 - y1^3 - k*y2 + B*cos(omega*t); p = [k, B, delta, omega]
+/// (duffing.hpp:37-42; same operation order).
+ODEGPU_HD ODEGPU_INLINE void duffing_rhs(Real t, std::span<const Real> y, std::span<const Real> p,
+                                         std::span<Real> dy) {
+    const Real k = p[0], B = p[1], delta = p[2], omega = p[3];
+    dy[0] = y[1];
+    dy[1] = delta * y[0] - y[0] * y[0] * y[0] - k * y[1] + B * cos(omega * t);
+}
+
+/// Duffing + linearised radius/angle (duffing.hpp:47-57).
+ODEGPU_HD ODEGPU_INLINE void duffing_lyapunov_rhs(Real t, std::span<const Real> y, std::span<const Real> p,
+                                                  std::span<Real> dy) {
+    duffing_rhs(t, y, p, dy);
+    const Real k = p[0], delta = p[2];
+    const Real g1 = delta - 3.0 * y[0] * y[0];
+    const Real g2 = -k;
+    Real s, c;
+#if defined(__CUDA_ARCH__)
+    sincos(y[3], &s, &c);
+#else
+    s = std::sin(y[3]);
+    c = std::cos(y[3]);
+#endif
+    dy[2] = y[2] * ((1.0 + g1) * s * c + g2 * s * s);
+    dy[3] = -s * s + (g1 * c + g2 * s) * c;
+}
+
+/// DuffingSystem (duffing.hpp:75-88): plain RHS.
+struct DuffingHooks : HookDefaults {
+    static constexpr Index kSystemDim = 2, kParamCount = 4, kEventCount = 0, kAccessoryCount = 0;
+    ODEGPU_HD void ode_rhs(Real t, std::span<const Real> y, std::span<const Real> p, std::span<Real> dy) const {
+        duffing_rhs(t, y, p, dy);
+    }
+};
+
+/// DuffingMaxAccessorySystem (duffing.hpp:92-117): running max of y1 + time.
+struct DuffingMaxAccessoryHooks : DuffingHooks {
+    static constexpr Index kAccessoryCount = 2;
+    ODEGPU_HD void initialize(Real t, std::span<Real>, std::span<Real> y, std::span<const Real>,
+                              std::span<Real> acc) const {
+        acc[0] = y[0];
+        acc[1] = t;
+    }
+    ODEGPU_HD void ordinary_accessory(Real t, std::span<const Real> y, std::span<const Real>,
+                                      std::span<Real> acc) const {
+        if (y[0] > acc[0]) {
+            acc[0] = y[0];
+            acc[1] = t;
+        }
+    }
+};
+
+/// DuffingMaxEventSystem (duffing.hpp:122-156): F = y2 falling locates the
+/// local maxima of y1; the event accessory keeps the largest and its time.
+struct DuffingMaxEventHooks : DuffingHooks {
+    static constexpr Index kEventCount = 1, kAccessoryCount = 2;
+    ODEGPU_HD void event_values(Real, std::span<const Real> y, std::span<const Real>, std::span<Real> f) const {
+        f[0] = y[1];
+    }
+    ODEGPU_HD void initialize(Real t, std::span<Real>, std::span<Real> y, std::span<const Real>,
+                              std::span<Real> acc) const {
+        acc[0] = y[0];
+        acc[1] = t;
+    }
+    ODEGPU_HD void event_accessory(Index event, Index, Real t, std::span<const Real> y, std::span<const Real>,
+                                   std::span<Real> acc) const {
+        if (event == 0 && y[0] > acc[0]) {
+            acc[0] = y[0];
+            acc[1] = t;
+        }
+    }
+};
+
+/// cfg1 harness model: per-period max and min of y1 with
+/// their times, acc = [y1_max, t_max, y1_min, t_min], seeded at t0.
+struct DuffingMaxMinHooks : DuffingHooks {
+    static constexpr Index kAccessoryCount = 4;
+    ODEGPU_HD void initialize(Real t, std::span<Real>, std::span<Real> y, std::span<const Real>,
+                              std::span<Real> acc) const {
+        acc[0] = y[0];
+        acc[1] = t;
+        acc[2] = y[0];
+        acc[3] = t;
+    }
+    ODEGPU_HD void ordinary_accessory(Real t, std::span<const Real> y, std::span<const Real>,
+                                      std::span<Real> acc) const {
+        if (y[0] > acc[0]) {
+            acc[0] = y[0];
+            acc[1] = t;
+        }
+        if (y[0] < acc[2]) {
+            acc[2] = y[0];
+            acc[3] = t;
+        }
+    }
+};
+
+/// DuffingLyapunovSystem (duffing.hpp:162-180): finalize samples the
+/// linearised radius into acc[0] and resets it to one.
+struct DuffingLyapunovHooks : HookDefaults {
+    static constexpr Index kSystemDim = 4, kParamCount = 4, kEventCount = 0, kAccessoryCount = 1;
+    ODEGPU_HD void ode_rhs(Real t, std::span<const Real> y, std::span<const Real> p, std::span<Real> dy) const {
+        duffing_lyapunov_rhs(t, y, p, dy);
+    }
+    ODEGPU_HD void finalize(Real, std::span<Real>, std::span<Real> y, std::span<const Real>,
+                            std::span<Real> acc) const {
+        acc[0] = y[2];
+        y[2] = 1.0;
+    }
+};
+
+} // namespace odegpu::models
+
+#endif

@@ -1,0 +1,88 @@
+// Keller-Miksis bubble models, hook side (device + host).
+// Restates /root/reference/proj/include/odensemble/models/keller_miksis.hpp.
+// The 13 coefficients are precomputed on the host (bubble_coefficients,
+// keller_miksis.hpp:47-77; see paper_1810_03931_b200/workloads.py and
+// include/odegpu/system.hpp) and are per-system parameters.
+#ifndef ODEGPU_MODELS_KELLER_MIKSIS_HPP
+#define ODEGPU_MODELS_KELLER_MIKSIS_HPP
+
+#include <cmath>
+#include <limits>
+#include <span>
+
+#include "odegpu/hooks.hpp"
+
+namespace odegpu::models {
+
+/// Dimensionless Keller-Miksis RHS (keller_miksis.hpp:82-103), same
+/// operation order. y1 <= 0 yields NaN derivatives for the step control.
+/// On the device sin/cos of the same argument share one range reduction
+/// (sincos), as the reference's g++ build merges them into glibc sincos.
+ODEGPU_HD ODEGPU_INLINE void keller_miksis_rhs(Real tau, std::span<const Real> y, std::span<const Real> c,
+                                               std::span<Real> dy) {
+    const Real y1 = y[0], y2 = y[1];
+    if (!(y1 > 0)) {
+        dy[0] = std::numeric_limits<Real>::quiet_NaN();
+        dy[1] = std::numeric_limits<Real>::quiet_NaN();
+        return;
+    }
+    constexpr Real two_pi = 2.0 * 3.141592653589793238462643383279502884;
+    const Real arg1 = two_pi * tau;
+    const Real arg2 = two_pi * c[11] * tau + c[12];
+    Real s1, c1, s2, c2;
+#if defined(__CUDA_ARCH__)
+    sincos(arg1, &s1, &c1);
+    sincos(arg2, &s2, &c2);
+#else
+    s1 = std::sin(arg1);
+    c1 = std::cos(arg1);
+    s2 = std::sin(arg2);
+    c2 = std::cos(arg2);
+#endif
+    const Real numerator = (c[0] + c[1] * y2) * pow(1.0 / y1, c[10]) - c[2] * (1.0 + c[9] * y2) - c[3] / y1 -
+                           c[4] * y2 / y1 - (1.0 - c[9] * y2 / 3.0) * 1.5 * y2 * y2 -
+                           (c[5] * s1 + c[6] * s2) * (1.0 + c[9] * y2) - y1 * (c[7] * c1 + c[8] * c2);
+    const Real denominator = y1 - c[9] * y1 * y2 + c[4] * c[9];
+    dy[0] = y2;
+    dy[1] = numerator / denominator;
+}
+
+/// KellerMiksisSystem (keller_miksis.hpp:106-119).
+struct KellerMiksisHooks : HookDefaults {
+    static constexpr Index kSystemDim = 2, kParamCount = 13, kEventCount = 0, kAccessoryCount = 0;
+    ODEGPU_HD void ode_rhs(Real t, std::span<const Real> y, std::span<const Real> p, std::span<Real> dy) const {
+        keller_miksis_rhs(t, y, p, dy);
+    }
+};
+
+/// BubbleCollapseSystem (keller_miksis.hpp:126-165): runs from one radius
+/// maximum to the next (F = y2 falling, stop at 1); acc = [tau_max, y1_max,
+/// tau_min, y1_min]; finalize moves t0 to the stop time.
+struct BubbleCollapseHooks : KellerMiksisHooks {
+    static constexpr Index kEventCount = 1, kAccessoryCount = 4;
+    ODEGPU_HD void event_values(Real, std::span<const Real> y, std::span<const Real>, std::span<Real> f) const {
+        f[0] = y[1];
+    }
+    ODEGPU_HD void initialize(Real t, std::span<Real>, std::span<Real> y, std::span<const Real>,
+                              std::span<Real> acc) const {
+        acc[0] = t;
+        acc[1] = y[0];
+        acc[2] = t;
+        acc[3] = y[0];
+    }
+    ODEGPU_HD void ordinary_accessory(Real t, std::span<const Real> y, std::span<const Real>,
+                                      std::span<Real> acc) const {
+        if (y[0] < acc[3]) {
+            acc[3] = y[0];
+            acc[2] = t;
+        }
+    }
+    ODEGPU_HD void finalize(Real t, std::span<Real> time_domain, std::span<Real>, std::span<const Real>,
+                            std::span<Real>) const {
+        time_domain[0] = t;
+    }
+};
+
+} // namespace odegpu::models
+
+#endif

@@ -1,0 +1,27 @@
+"""odegpu — B200-native ensemble ODE solver (hot path of arXiv 1810.03931).
+
+The compute path is libodegpu.so (hand-written sm_100a CUDA behind the C ABI
+in include/odegpu.h). This package is the thin host mirror used by tests and
+bench.py; the C++ host API lives in include/odegpu/.
+"""
+from . import abi, models, workloads  # noqa: F401
+from .api import (  # noqa: F401
+    BatchDims,
+    CopyMode,
+    InvalidArgument,
+    LinearCopySpec,
+    OdegpuError,
+    OutOfRange,
+    PoolDims,
+    ProblemPool,
+    RandomCopySpec,
+    SolverBatch,
+    SolverConfig,
+    dfma_peak,
+    flat_index,
+    linear_set,
+    make_batch_dims,
+    random_set,
+    solve,
+    solve_iteratively,
+)

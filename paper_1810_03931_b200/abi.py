@@ -1,0 +1,230 @@
+"""ctypes mirror of include/odegpu.h (the C ABI of libodegpu).
+
+Only plain structs and the loader live here. The library is built in-tree by
+``__graft_entry__.build()`` (``paper_1810_03931_b200/lib/libodegpu.so``); on a
+machine with a GPU a missing library is an error — there is no fallback path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+PKG_DIR = Path(__file__).resolve().parent
+LIB_DIR = PKG_DIR / "lib"
+LIB_PATH = LIB_DIR / "libodegpu.so"
+
+# include/odegpu.h constants
+OK = 0
+ERR_INVALID_ARGUMENT = -1
+ERR_OUT_OF_RANGE = -2
+ERR_CUDA = -3
+ERR_UNSUPPORTED = -4
+
+RK4, RKCK45 = 0, 1
+REACHED_END_TIME, EVENT_STOP, EQUILIBRIUM_STOP, NONFINITE_ABORT = 0, 1, 2, 3
+COPY_TIME_DOMAIN, COPY_ACTUAL_STATE, COPY_PARAMETER, COPY_ACCESSORIES, COPY_ALL = 0, 1, 2, 3, 4
+PROP_TIME_DOMAIN, PROP_STATE, PROP_PARAMETERS, PROP_ACCESSORIES = 0, 1, 2, 3
+
+MODEL_DUFFING = 0
+MODEL_DUFFING_MAX_ACCESSORY = 1
+MODEL_DUFFING_MAX_EVENT = 2
+MODEL_DUFFING_MAXMIN = 3
+MODEL_KELLER_MIKSIS = 4
+MODEL_BUBBLE_COLLAPSE = 5
+MODEL_VALVE = 6
+MODEL_DUFFING_LYAPUNOV = 7
+MODEL_CONSTANT = 16
+MODEL_CUBIC_TIME = 17
+MODEL_EXPONENTIAL = 18
+MODEL_UNIT_SLOPE = 19
+MODEL_COUNTING = 20
+MODEL_RAMP = 21
+MODEL_DECAY = 22
+MODEL_SEAT_CONTACT = 23
+MODEL_HARMONIC = 24
+MODEL_BLOWUP = 25
+
+MAX_MODEL_CONSTS = 8
+
+Index = C.c_int64
+
+
+class Model(C.Structure):
+    _fields_ = [("id", C.c_int32), ("reserved", C.c_int32), ("consts", C.c_double * MAX_MODEL_CONSTS)]
+
+
+class SystemDims(C.Structure):
+    _fields_ = [("system_dim", Index), ("param_count", Index), ("event_count", Index), ("accessory_count", Index)]
+
+
+class PoolDims(C.Structure):
+    _fields_ = [("problem_size", Index), ("system_dim", Index), ("param_count", Index), ("accessory_count", Index)]
+
+
+class BatchDims(C.Structure):
+    _fields_ = [
+        ("batch_capacity", Index),
+        ("system_dim", Index),
+        ("param_count", Index),
+        ("event_count", Index),
+        ("accessory_count", Index),
+    ]
+
+
+class PoolView(C.Structure):
+    _fields_ = [
+        ("dims", PoolDims),
+        ("time_domain", C.POINTER(C.c_double)),
+        ("state", C.POINTER(C.c_double)),
+        ("parameters", C.POINTER(C.c_double)),
+        ("accessories", C.POINTER(C.c_double)),
+    ]
+
+
+class LinearCopySpec(C.Structure):
+    _fields_ = [
+        ("start_in_batch", Index),
+        ("start_in_pool", Index),
+        ("element_count", Index),
+        ("copy_mode", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+
+class SolverConfig(C.Structure):
+    _fields_ = [
+        ("algorithm", C.c_int32),
+        ("reserved", C.c_int32),
+        ("initial_time_step", C.c_double),
+        ("tile_size", Index),
+        ("worker_count", Index),
+    ]
+
+
+class OdeControls(C.Structure):
+    _fields_ = [
+        ("rel_tol", C.POINTER(C.c_double)),
+        ("abs_tol", C.POINTER(C.c_double)),
+        ("max_step", C.c_double),
+        ("min_step", C.c_double),
+        ("step_grow_limit", C.c_double),
+        ("step_shrink_limit", C.c_double),
+    ]
+
+
+class EventControls(C.Structure):
+    _fields_ = [
+        ("direction", C.POINTER(C.c_int32)),
+        ("tolerance", C.POINTER(C.c_double)),
+        ("stop_condition", C.POINTER(Index)),
+        ("max_steps_in_zone", Index),
+    ]
+
+
+# odegpu_outcome / odensemble::SystemOutcome (driver.hpp:34-42), 56 bytes.
+OUTCOME_DTYPE = np.dtype(
+    {
+        "names": [
+            "final_t",
+            "reason",
+            "accepted_steps",
+            "rejected_steps",
+            "event_detections",
+            "secant_failures",
+            "smallest_step",
+        ],
+        "formats": ["<f8", "u1", "<i8", "<i8", "<i8", "<i8", "<f8"],
+        "offsets": [0, 8, 16, 24, 32, 40, 48],
+        "itemsize": 56,
+    }
+)
+
+SINK = C.CFUNCTYPE(C.c_int, Index, C.c_void_p, C.c_void_p)
+
+
+def dptr(a: np.ndarray | None):
+    if a is None:
+        return C.POINTER(C.c_double)()
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def vptr(a: np.ndarray | None):
+    if a is None:
+        return C.c_void_p()
+    assert a.flags.c_contiguous
+    return C.c_void_p(a.ctypes.data)
+
+
+def empty_outcomes(n: int) -> np.ndarray:
+    o = np.zeros(n, dtype=OUTCOME_DTYPE)
+    o["smallest_step"] = np.inf
+    return o
+
+
+class LibraryMissing(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def _bind(lib):
+    P = C.POINTER
+    vp = C.c_void_p
+    sig = {
+        "odegpu_abi_version": (C.c_int, []),
+        "odegpu_last_error": (C.c_char_p, []),
+        "odegpu_device_count": (C.c_int, []),
+        "odegpu_model_dims": (C.c_int, [P(Model), P(SystemDims)]),
+        "odegpu_batch_create": (C.c_int, [P(BatchDims), C.c_int, P(vp)]),
+        "odegpu_batch_destroy": (None, [vp]),
+        "odegpu_batch_dims_get": (C.c_int, [vp, P(BatchDims)]),
+        "odegpu_batch_set_stream": (C.c_int, [vp, vp]),
+        "odegpu_linear_set": (C.c_int, [vp, P(PoolView), P(LinearCopySpec)]),
+        "odegpu_random_set": (C.c_int, [vp, P(PoolView), P(Index), P(Index), Index, C.c_int32]),
+        "odegpu_batch_read": (C.c_int, [vp, C.c_int32, P(C.c_double)]),
+        "odegpu_batch_write": (C.c_int, [vp, C.c_int32, P(C.c_double)]),
+        "odegpu_batch_read_range": (C.c_int, [vp, C.c_int32, Index, Index, P(C.c_double), Index]),
+        "odegpu_batch_write_range": (C.c_int, [vp, C.c_int32, Index, Index, P(C.c_double), Index]),
+        "odegpu_batch_read_outcomes": (C.c_int, [vp, vp]),
+        "odegpu_batch_write_outcomes": (C.c_int, [vp, vp]),
+        "odegpu_batch_reset_outcomes": (C.c_int, [vp]),
+        "odegpu_solve": (C.c_int, [vp, P(Model), P(SolverConfig), P(OdeControls), P(EventControls)]),
+        "odegpu_solve_iteratively": (
+            C.c_int,
+            [vp, P(Model), P(SolverConfig), P(OdeControls), P(EventControls), Index, SINK, vp],
+        ),
+        "odegpu_batch_sync": (C.c_int, [vp]),
+        "odegpu_batch_launch_count": (C.c_int64, [vp]),
+        "odegpu_dfma_peak": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, P(C.c_double), P(C.c_double)]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+def exported_symbols() -> list[str]:
+    """Every function include/odegpu.h declares (parsed from the header)."""
+    import re
+
+    hdr = (PKG_DIR.parent / "include" / "odegpu.h").read_text()
+    return sorted(set(re.findall(r"^\w[\w\s\*]*?\b(odegpu_\w+)\s*\(", hdr, flags=re.M)))
+
+
+def load() -> C.CDLL:
+    """Load the in-tree libodegpu.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        path = Path(os.environ.get("ODEGPU_LIB", LIB_PATH))
+        if not path.exists():
+            raise LibraryMissing(
+                f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        _lib = _bind(C.CDLL(str(path)))
+    return _lib

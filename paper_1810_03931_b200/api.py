@@ -1,0 +1,380 @@
+"""Python mirror of the reference's pool / batch / solve API over the C ABI.
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/include/odensemble/{pool,batch,solve}.hpp, so parity
+tests read like the reference's own tests. All compute goes through
+libodegpu (include/odegpu.h); there is no CPU path here.
+
+Errors: the reference's std::invalid_argument maps to InvalidArgument
+(a ValueError), std::out_of_range to OutOfRange (an IndexError).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import abi
+from .models import SystemDef, SystemDims
+
+
+class OdegpuError(RuntimeError):
+    code = abi.ERR_CUDA
+
+
+class InvalidArgument(OdegpuError, ValueError):
+    code = abi.ERR_INVALID_ARGUMENT
+
+
+class OutOfRange(OdegpuError, IndexError):
+    code = abi.ERR_OUT_OF_RANGE
+
+
+class Unsupported(OdegpuError):
+    code = abi.ERR_UNSUPPORTED
+
+
+_ERRORS = {abi.ERR_INVALID_ARGUMENT: InvalidArgument, abi.ERR_OUT_OF_RANGE: OutOfRange,
+           abi.ERR_UNSUPPORTED: Unsupported}
+
+
+def check(rc: int):
+    if rc != 0:
+        msg = abi.load().odegpu_last_error().decode()
+        raise _ERRORS.get(rc, OdegpuError)(msg)
+
+
+Algorithm_RK4, Algorithm_RKCK45 = abi.RK4, abi.RKCK45
+
+
+@dataclass
+class SolverConfig:
+    """driver.hpp:25-30."""
+
+    algorithm: int = abi.RKCK45
+    initial_time_step: float = 1e-3
+    tile_size: int = 64
+    worker_count: int = 1
+
+    def to_c(self):
+        return abi.SolverConfig(self.algorithm, 0, self.initial_time_step, self.tile_size, self.worker_count)
+
+
+@dataclass
+class PoolDims:
+    problem_size: int
+    system_dim: int
+    param_count: int
+    accessory_count: int
+
+    def validate(self):  # pool.hpp:51-56
+        if self.problem_size < 1:
+            raise InvalidArgument("PoolDims: problem_size must be >= 1")
+        if self.system_dim < 1:
+            raise InvalidArgument("PoolDims: system_dim must be >= 1")
+        if self.param_count < 0:
+            raise InvalidArgument("PoolDims: param_count must be >= 0")
+        if self.accessory_count < 0:
+            raise InvalidArgument("PoolDims: accessory_count must be >= 0")
+
+
+@dataclass
+class BatchDims:
+    batch_capacity: int
+    system_dim: int
+    param_count: int
+    event_count: int
+    accessory_count: int
+
+    def to_c(self):
+        return abi.BatchDims(self.batch_capacity, self.system_dim, self.param_count, self.event_count,
+                             self.accessory_count)
+
+
+def make_batch_dims(capacity: int, sys: SystemDims) -> BatchDims:
+    """pool.hpp:65-69."""
+    return BatchDims(capacity, sys.system_dim, sys.param_count, sys.event_count, sys.accessory_count)
+
+
+def flat_index(idx: int, component: int, count: int) -> int:
+    """pool.hpp:16-23."""
+    if idx < 0 or idx >= count:
+        raise OutOfRange(f"flat_index: system index {idx} outside [0, {count})")
+    if component < 0:
+        raise OutOfRange("flat_index: negative component index")
+    return idx + component * count
+
+
+class ProblemPool:
+    """Host pool in SoA layout (pool.hpp:74-139). Arrays are numpy views."""
+
+    def __init__(self, dims: PoolDims):
+        dims.validate()
+        self.dims = dims
+        n = dims.problem_size
+        self._td = np.zeros(2 * n)
+        self._state = np.zeros(dims.system_dim * n)
+        self._params = np.zeros(dims.param_count * n)
+        self._acc = np.zeros(dims.accessory_count * n)
+
+    def size(self):
+        return self.dims.problem_size
+
+    def time_domain(self):
+        return self._td
+
+    def state(self):
+        return self._state
+
+    def parameters(self):
+        return self._params
+
+    def accessories(self):
+        return self._acc
+
+    def _check(self, c, count, what):
+        if c < 0 or c >= count:
+            raise OutOfRange(f"ProblemPool: {what} component out of range")
+
+    def set_time(self, idx, t0, t1):
+        n = self.size()
+        self._td[flat_index(idx, 0, n)] = t0
+        self._td[flat_index(idx, 1, n)] = t1
+
+    def time_start(self, idx):
+        return self._td[flat_index(idx, 0, self.size())]
+
+    def time_end(self, idx):
+        return self._td[flat_index(idx, 1, self.size())]
+
+    def state_at(self, idx, c):
+        self._check(c, self.dims.system_dim, "state")
+        return self._state[flat_index(idx, c, self.size())]
+
+    def set_state(self, idx, c, v):
+        self._check(c, self.dims.system_dim, "state")
+        self._state[flat_index(idx, c, self.size())] = v
+
+    def param_at(self, idx, c):
+        self._check(c, self.dims.param_count, "parameter")
+        return self._params[flat_index(idx, c, self.size())]
+
+    def set_param(self, idx, c, v):
+        self._check(c, self.dims.param_count, "parameter")
+        self._params[flat_index(idx, c, self.size())] = v
+
+    def accessory_at(self, idx, c):
+        self._check(c, self.dims.accessory_count, "accessory")
+        return self._acc[flat_index(idx, c, self.size())]
+
+    def set_accessory(self, idx, c, v):
+        self._check(c, self.dims.accessory_count, "accessory")
+        self._acc[flat_index(idx, c, self.size())] = v
+
+    def view(self):
+        v = abi.PoolView(
+            abi.PoolDims(self.dims.problem_size, self.dims.system_dim, self.dims.param_count,
+                         self.dims.accessory_count),
+            abi.dptr(self._td), abi.dptr(self._state), abi.dptr(self._params if self._params.size else None),
+            abi.dptr(self._acc if self._acc.size else None))
+        v._keep = self
+        return v
+
+    @staticmethod
+    def from_arrays(td, y, p, acc) -> "ProblemPool":
+        """Pool over flat SoA arrays (copied)."""
+        n = td.size // 2
+        pool = ProblemPool(PoolDims(n, y.size // n, p.size // n, acc.size // n))
+        pool._td[:] = td
+        pool._state[:] = y
+        pool._params[:] = p
+        pool._acc[:] = acc
+        return pool
+
+
+# CopyMode (pool.hpp:142)
+class CopyMode:
+    TimeDomain, ActualState, Parameter, Accessories, All = (abi.COPY_TIME_DOMAIN, abi.COPY_ACTUAL_STATE,
+                                                            abi.COPY_PARAMETER, abi.COPY_ACCESSORIES, abi.COPY_ALL)
+
+
+@dataclass
+class LinearCopySpec:
+    start_in_batch: int = 0
+    start_in_pool: int = 0
+    element_count: int = 0
+    copy_mode: int = CopyMode.All
+
+
+@dataclass
+class RandomCopySpec:
+    indices_in_batch: list
+    indices_in_pool: list
+    copy_mode: int = CopyMode.All
+
+
+class SolverBatch:
+    """Device-resident batch (batch.hpp:17-67) on one GPU. Accessors copy the
+    device arrays back (D2H) — the lazy host mirror of the reference's
+    spans."""
+
+    def __init__(self, dims: BatchDims, device: int = 0):
+        self._lib = abi.load()
+        self.dims = dims
+        self.device = device
+        h = C.c_void_p()
+        check(self._lib.odegpu_batch_create(C.byref(dims.to_c()), device, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.odegpu_batch_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def size(self):
+        return self.dims.batch_capacity
+
+    def _read(self, prop, comps):
+        out = np.zeros(comps * self.size())
+        if comps:
+            check(self._lib.odegpu_batch_read(self._h, prop, abi.dptr(out)))
+        return out
+
+    def _write(self, prop, arr):
+        arr = np.ascontiguousarray(arr, dtype=np.float64)
+        check(self._lib.odegpu_batch_write(self._h, prop, abi.dptr(arr)))
+
+    def time_domain(self):
+        return self._read(abi.PROP_TIME_DOMAIN, 2)
+
+    def state(self):
+        return self._read(abi.PROP_STATE, self.dims.system_dim)
+
+    def parameters(self):
+        return self._read(abi.PROP_PARAMETERS, self.dims.param_count)
+
+    def accessories(self):
+        return self._read(abi.PROP_ACCESSORIES, self.dims.accessory_count)
+
+    def set_time_domain(self, a):
+        self._write(abi.PROP_TIME_DOMAIN, a)
+
+    def set_state(self, a):
+        self._write(abi.PROP_STATE, a)
+
+    def set_parameters(self, a):
+        self._write(abi.PROP_PARAMETERS, a)
+
+    def set_accessories(self, a):
+        self._write(abi.PROP_ACCESSORIES, a)
+
+    def outcomes(self) -> np.ndarray:
+        out = np.zeros(self.size(), dtype=abi.OUTCOME_DTYPE)
+        check(self._lib.odegpu_batch_read_outcomes(self._h, abi.vptr(out)))
+        return out
+
+    def set_outcomes(self, o: np.ndarray):
+        o = np.ascontiguousarray(o, dtype=abi.OUTCOME_DTYPE)
+        check(self._lib.odegpu_batch_write_outcomes(self._h, abi.vptr(o)))
+
+    def reset_outcomes(self):
+        check(self._lib.odegpu_batch_reset_outcomes(self._h))
+
+    def time_start(self, i):
+        return self.time_domain()[flat_index(i, 0, self.size())]
+
+    def time_end(self, i):
+        return self.time_domain()[flat_index(i, 1, self.size())]
+
+    def state_at(self, i, c):
+        return self.state()[flat_index(i, c, self.size())]
+
+    def param_at(self, i, c):
+        return self.parameters()[flat_index(i, c, self.size())]
+
+    def accessory_at(self, i, c):
+        return self.accessories()[flat_index(i, c, self.size())]
+
+    def set_stream(self, stream_handle: int | None):
+        check(self._lib.odegpu_batch_set_stream(self._h, C.c_void_p(stream_handle or 0)))
+
+    def sync(self):
+        check(self._lib.odegpu_batch_sync(self._h))
+
+    def launch_count(self) -> int:
+        return int(self._lib.odegpu_batch_launch_count(self._h))
+
+
+def linear_set(batch: SolverBatch, pool: ProblemPool, spec: LinearCopySpec):
+    """batch.cpp:78-104."""
+    c = abi.LinearCopySpec(spec.start_in_batch, spec.start_in_pool, spec.element_count, spec.copy_mode, 0)
+    check(batch._lib.odegpu_linear_set(batch.handle, C.byref(pool.view()), C.byref(c)))
+
+
+def random_set(batch: SolverBatch, pool: ProblemPool, spec: RandomCopySpec):
+    """batch.cpp:106-135."""
+    ib = np.ascontiguousarray(spec.indices_in_batch, dtype=np.int64)
+    ip = np.ascontiguousarray(spec.indices_in_pool, dtype=np.int64)
+    if ib.size != ip.size:
+        raise InvalidArgument("random_set: index lists differ in length")
+    P = C.POINTER(C.c_int64)
+    check(batch._lib.odegpu_random_set(batch.handle, C.byref(pool.view()), ib.ctypes.data_as(P),
+                                       ip.ctypes.data_as(P), ib.size, spec.copy_mode))
+
+
+def _controls(defn: SystemDef):
+    ode = defn.ode_controls().to_c()
+    ev = defn.event_controls().to_c()
+    return ode, ev
+
+
+def solve(batch: SolverBatch, defn: SystemDef, cfg: SolverConfig | None = None):
+    """solve.hpp:60-128 — synchronous, in place."""
+    cfg = cfg or SolverConfig()
+    ode, ev = _controls(defn)
+    check(batch._lib.odegpu_solve(batch.handle, C.byref(defn.to_c()), C.byref(cfg.to_c()), C.byref(ode),
+                                  C.byref(ev)))
+
+
+def solve_iteratively(batch: SolverBatch, defn: SystemDef, cfg: SolverConfig | None, iterations: int, sink=None):
+    """solve.hpp:133-142. sink(iteration, batch) after each solve; with no
+    sink the iterations run back to back on the device."""
+    cfg = cfg or SolverConfig()
+    ode, ev = _controls(defn)
+    err = []
+
+    def _sink(it, _h, _u):
+        try:
+            sink(int(it), batch)
+            return 0
+        except BaseException as e:  # propagate after the C loop unwinds
+            err.append(e)
+            return 1
+
+    cb = abi.SINK(_sink) if sink else abi.SINK()
+    rc = batch._lib.odegpu_solve_iteratively(batch.handle, C.byref(defn.to_c()), C.byref(cfg.to_c()),
+                                             C.byref(ode), C.byref(ev), int(iterations), cb, None)
+    if err:
+        raise err[0]
+    check(rc)
+
+
+def dfma_peak(device: int = 0, blocks: int | None = None, threads: int = 256, iters: int = 4096):
+    """Lane-DFMA/s of the FP64 pipe measured by the microbenchmark kernel."""
+    lib = abi.load()
+    if blocks is None:
+        blocks = 148 * 16
+    rate, secs = C.c_double(), C.c_double()
+    check(lib.odegpu_dfma_peak(device, blocks, threads, iters, C.byref(rate), C.byref(secs)))
+    return rate.value, secs.value

@@ -1,0 +1,105 @@
+"""Parity helpers shared by the GPU tests, smoke() and the parity report.
+
+Runs a workload through the product (C ABI) and through a CPU checker on the
+same inputs and compares with the rules of SURVEY.md §8(c):
+* exact: accepted / rejected steps, event detections, stop reason, secant failures;
+* <= rtol relative (absolute floor `atol`) on state, accessories, td, final_t;
+* components pinned by a stop event (|F| <= event tol at the stop) compared
+  with |d| <= 2 * event_tol instead;
+* time-of-extremum accessories: within one local step (smallest_step) when
+  the matching value accessory agrees.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+import paper_1810_03931_b200 as pkg
+from paper_1810_03931_b200 import abi
+
+COUNT_FIELDS = ("accepted_steps", "rejected_steps", "event_detections", "reason", "secant_failures")
+
+
+def run_gpu(wl, iterations: int, device: int = 0, trace: bool = False):
+    td, y, p, acc = wl.arrays()
+    pool = pkg.ProblemPool.from_arrays(td, y, p, acc)
+    batch = pkg.SolverBatch(pkg.make_batch_dims(wl.n, wl.model.dims()), device=device)
+    pkg.linear_set(batch, pool, pkg.LinearCopySpec(0, 0, wl.n))
+    cfg = pkg.SolverConfig(wl.algorithm, wl.dt)
+    tr = [] if trace else None
+
+    def sink(it, b):
+        tr.append(dict(td=b.time_domain(), y=b.state(), acc=b.accessories(), outcomes=b.outcomes()))
+
+    pkg.solve_iteratively(batch, wl.model, cfg, iterations, sink if trace else None)
+    out = dict(td=batch.time_domain(), y=batch.state(), acc=batch.accessories(), outcomes=batch.outcomes(),
+               launches=batch.launch_count(), trace=tr)
+    batch.close()
+    return out
+
+
+def rel_err(a, b, atol):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    both_nan = np.isnan(a) & np.isnan(b)
+    same_inf = np.isinf(a) & np.isinf(b) & (np.sign(a) == np.sign(b))
+    d = np.abs(a - b) / (np.abs(b) + atol)
+    d[both_nan | same_inf] = 0.0
+    d[np.isnan(d)] = np.inf
+    return d
+
+
+def compare(wl, gpu, ref, *, pinned_state=(), pinned_acc=(), time_acc=()) -> dict:
+    """Per-field statistics; `pinned_*` are component indices compared with
+    the event-tolerance rule, `time_acc` maps time-accessory -> value-accessory."""
+    n = wl.n
+    d = wl.model.dims()
+    og, orf = gpu["outcomes"], ref["outcomes"]
+    rep = {"n": n}
+    for k in COUNT_FIELDS:
+        rep[f"mismatch_{k}"] = int(np.count_nonzero(og[k] != orf[k]))
+    atol = float(min(wl.model.ode_controls().abs_tol))
+    ev_tol = max(wl.model.event_controls().tolerance or [0.0])
+    stopped = orf["reason"] == abi.EVENT_STOP
+    y_g = gpu["y"].reshape(d.system_dim, n)
+    y_r = ref["y"].reshape(d.system_dim, n)
+    worst = 0.0
+    for c in range(d.system_dim):
+        if c in pinned_state:
+            e = np.abs(y_g[c] - y_r[c])
+            rep[f"y{c}_pinned_abs"] = float(np.max(np.where(stopped, e, 0.0))) if n else 0.0
+            free = ~stopped
+            rep[f"y{c}_rel"] = float(np.max(rel_err(y_g[c][free], y_r[c][free], atol), initial=0.0))
+        else:
+            rep[f"y{c}_rel"] = float(np.max(rel_err(y_g[c], y_r[c], atol), initial=0.0))
+        worst = max(worst, rep[f"y{c}_rel"])
+    a_g = gpu["acc"].reshape(max(d.accessory_count, 1), n) if d.accessory_count else None
+    a_r = ref["acc"].reshape(max(d.accessory_count, 1), n) if d.accessory_count else None
+    for c in range(d.accessory_count):
+        if c in time_acc:
+            vc = time_acc[c]
+            same_val = rel_err(a_g[vc], a_r[vc], atol) <= 1e-9
+            step = np.where(np.isfinite(orf["smallest_step"]), orf["smallest_step"], 0.0)
+            dt = np.abs(a_g[c] - a_r[c])
+            rep[f"acc{c}_time_steps_off"] = int(np.count_nonzero(same_val & (dt > step * 1.000001 + 1e-15)))
+            rep[f"acc{c}_rel"] = float(np.max(rel_err(a_g[c], a_r[c], atol), initial=0.0))
+        elif c in pinned_acc:
+            rep[f"acc{c}_pinned_abs"] = float(np.max(np.abs(a_g[c] - a_r[c]), initial=0.0))
+        else:
+            rep[f"acc{c}_rel"] = float(np.max(rel_err(a_g[c], a_r[c], atol), initial=0.0))
+            worst = max(worst, rep[f"acc{c}_rel"])
+    rep["td_rel"] = float(np.max(rel_err(gpu["td"], ref["td"], atol), initial=0.0))
+    rep["final_t_rel"] = float(np.max(rel_err(og["final_t"], orf["final_t"], atol), initial=0.0))
+    rep["event_tol"] = ev_tol
+    rep["worst_rel"] = worst
+    rep["steps"] = int(orf["accepted_steps"].sum() + orf["rejected_steps"].sum())
+    return rep
+
+
+# Per-config comparison rules: which components a stop event
+# pins, which accessories are times of extrema.
+RULES = {
+    "cfg1_duffing_rk4": dict(time_acc={1: 0, 3: 2}),
+    "cfg2_duffing_rkck45_event": dict(time_acc={1: 0}),
+    "cfg3_keller_miksis": dict(pinned_state=(1,), time_acc={0: 1, 2: 3}),
+    "cfg4_valve": dict(pinned_state=(1,), time_acc={}),
+}
