@@ -21,6 +21,7 @@
 #include "odensemble/models/duffing.hpp"
 #include "odensemble/models/keller_miksis.hpp"
 #include "odensemble/models/valve.hpp"
+#include "odensemble/scan.hpp"
 #include "odensemble/solve.hpp"
 
 using namespace odensemble;
@@ -295,6 +296,19 @@ int odref_bubble_coefficients(odegpu_index n, const double* phys, double* out) {
             const auto c = models::bubble_coefficients(b);
             for (Index k = 0; k < 13; ++k) out[i + k * n] = c[static_cast<std::size_t>(k)];
         }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return ODEGPU_ERR_INVALID_ARGUMENT;
+    }
+}
+
+// scan::ParamRange::values (src/scan.cpp:17-37) -> out[res].
+int odref_param_range(double lo, double hi, odegpu_index res, int log_scale, double* out) {
+    try {
+        scan::ParamRange r{lo, hi, res, log_scale ? scan::Scale::Log : scan::Scale::Linear};
+        const auto v = r.values();
+        std::copy(v.begin(), v.end(), out);
         return 0;
     } catch (const std::exception& e) {
         g_err = e.what();

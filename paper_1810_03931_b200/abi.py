@@ -142,6 +142,17 @@ OUTCOME_DTYPE = np.dtype(
     }
 )
 
+class Diagnostics(C.Structure):
+    _fields_ = [
+        ("accepted_steps", Index),
+        ("rejected_steps", Index),
+        ("event_detections", Index),
+        ("secant_failures", Index),
+        ("reason_counts", Index * 4),
+        ("max_trial_steps", Index),
+    ]
+
+
 SINK = C.CFUNCTYPE(C.c_int, Index, C.c_void_p, C.c_void_p)
 
 
@@ -200,6 +211,8 @@ def _bind(lib):
         ),
         "odegpu_batch_sync": (C.c_int, [vp]),
         "odegpu_batch_launch_count": (C.c_int64, [vp]),
+        "odegpu_batch_diagnostics": (C.c_int, [vp, P(Diagnostics)]),
+        "odegpu_batch_last_kernel_ms": (C.c_int, [vp, P(C.c_double)]),
         "odegpu_dfma_peak": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, P(C.c_double), P(C.c_double)]),
     }
     for name, (res, args) in sig.items():

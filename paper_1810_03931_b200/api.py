@@ -315,6 +315,19 @@ class SolverBatch:
     def launch_count(self) -> int:
         return int(self._lib.odegpu_batch_launch_count(self._h))
 
+    def diagnostics(self) -> dict:
+        """Device-side tally of the last solve's outcomes."""
+        d = abi.Diagnostics()
+        check(self._lib.odegpu_batch_diagnostics(self._h, C.byref(d)))
+        return dict(accepted_steps=d.accepted_steps, rejected_steps=d.rejected_steps,
+                    event_detections=d.event_detections, secant_failures=d.secant_failures,
+                    reason_counts=list(d.reason_counts), max_trial_steps=d.max_trial_steps)
+
+    def last_kernel_ms(self) -> float:
+        v = C.c_double()
+        check(self._lib.odegpu_batch_last_kernel_ms(self._h, C.byref(v)))
+        return v.value
+
 
 def linear_set(batch: SolverBatch, pool: ProblemPool, spec: LinearCopySpec):
     """batch.cpp:78-104."""

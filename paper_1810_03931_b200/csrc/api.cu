@@ -120,6 +120,43 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     dev::solve_lanes<H, ALG>(model, b, c);
 }
 
+// Outcome tally (ScanDiagnostics::tally_iteration, src/scan.cpp:63-68).
+// acc[0..3] = sums, acc[4..7] = reason counts, acc[8] = max trial steps.
+__global__ void diagnostics_kernel(dev::BatchArrays b, unsigned long long* acc) {
+    unsigned long long s_acc = 0, s_rej = 0, s_det = 0, s_sf = 0, r[4] = {0, 0, 0, 0}, mx = 0;
+    for (Index i = blockIdx.x * static_cast<Index>(blockDim.x) + threadIdx.x; i < b.n;
+         i += static_cast<Index>(gridDim.x) * blockDim.x) {
+        s_acc += b.accepted[i];
+        s_rej += b.rejected[i];
+        s_det += b.detections[i];
+        s_sf += b.secant_failures[i];
+        const unsigned rs = b.reason[i] & 3u;
+        r[0] += rs == 0;
+        r[1] += rs == 1;
+        r[2] += rs == 2;
+        r[3] += rs == 3;
+        const unsigned long long tr = static_cast<unsigned long long>(b.accepted[i] + b.rejected[i]);
+        mx = tr > mx ? tr : mx;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        s_acc += __shfl_down_sync(0xffffffffu, s_acc, o);
+        s_rej += __shfl_down_sync(0xffffffffu, s_rej, o);
+        s_det += __shfl_down_sync(0xffffffffu, s_det, o);
+        s_sf += __shfl_down_sync(0xffffffffu, s_sf, o);
+        for (int k = 0; k < 4; ++k) r[k] += __shfl_down_sync(0xffffffffu, r[k], o);
+        const unsigned long long m2 = __shfl_down_sync(0xffffffffu, mx, o);
+        mx = m2 > mx ? m2 : mx;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(acc + 0, s_acc);
+        atomicAdd(acc + 1, s_rej);
+        atomicAdd(acc + 2, s_det);
+        atomicAdd(acc + 3, s_sf);
+        for (int k = 0; k < 4; ++k) atomicAdd(acc + 4 + k, r[k]);
+        atomicMax(acc + 8, mx);
+    }
+}
+
 // FP64 peak microbenchmark: 8 independent DFMA chains per thread.
 __global__ void dfma_peak_kernel(double* out, int iters, double seed) {
     double a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
@@ -154,6 +191,9 @@ struct odegpu_batch {
     dev::BatchArrays a{};
     unsigned long long* first_bad = nullptr; // solve-time validation result
     unsigned long long* host_flag = nullptr;  // pinned mirror of first_bad
+    unsigned long long* diag = nullptr;       // device tally (9 counters)
+    cudaEvent_t ev_start = nullptr, ev_stop = nullptr; // brackets the last solve kernel
+    bool timed = false;
     int num_sms = 0;
     int64_t launches = 0;
     void* block = nullptr; // single device allocation backing every array
@@ -268,8 +308,11 @@ void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
     const Index needed = (n + kBlock - 1) / kBlock;
     const int grid = static_cast<int>(std::max<Index>(1, std::min(needed, persistent)));
     CK(cudaMemsetAsync(b->a.work, 0, sizeof(unsigned long long), b->stream));
+    CK(cudaEventRecord(b->ev_start, b->stream));
     kern<<<grid, kBlock, 0, b->stream>>>(hooks, b->a, c, b->first_bad);
     CK(cudaGetLastError());
+    CK(cudaEventRecord(b->ev_stop, b->stream));
+    b->timed = true;
     ++b->launches;
 }
 
@@ -435,14 +478,14 @@ int odegpu_batch_create(const odegpu_batch_dims* dims, int device, odegpu_batch*
                 n,                                         // reason
                 n * 8, n * 8, n * 8, n * 8,                // counters
                 n * 8,                                     // smallest
-                8, 8};                                     // work, first_bad
+                8, 8, 128};                                // work, first_bad, diag
             size_t total = 0;
             for (size_t s : sizes) total += align_up(s);
             CK(cudaMalloc(&b->block, total));
             CK(cudaMemsetAsync(b->block, 0, total, b->stream));
             char* p = static_cast<char*>(b->block);
-            void* ptrs[13];
-            for (int i = 0; i < 13; ++i) {
+            void* ptrs[14];
+            for (int i = 0; i < 14; ++i) {
                 ptrs[i] = p;
                 p += align_up(sizes[i]);
             }
@@ -459,6 +502,9 @@ int odegpu_batch_create(const odegpu_batch_dims* dims, int device, odegpu_batch*
             b->a.smallest_step = static_cast<Real*>(ptrs[10]);
             b->a.work = static_cast<unsigned long long*>(ptrs[11]);
             b->first_bad = static_cast<unsigned long long*>(ptrs[12]);
+            b->diag = static_cast<unsigned long long*>(ptrs[13]);
+            CK(cudaEventCreate(&b->ev_start));
+            CK(cudaEventCreate(&b->ev_stop));
             b->a.n = dims->batch_capacity;
             CK(cudaMallocHost(&b->host_flag, sizeof(unsigned long long)));
             reset_outcomes_kernel<<<grid_for(b, dims->batch_capacity, 256), 256, 0, b->stream>>>(
@@ -481,6 +527,8 @@ void odegpu_batch_destroy(odegpu_batch* b) {
     if (b->stream) cudaStreamSynchronize(b->stream);
     if (b->block) cudaFree(b->block);
     if (b->host_flag) cudaFreeHost(b->host_flag);
+    if (b->ev_start) cudaEventDestroy(b->ev_start);
+    if (b->ev_stop) cudaEventDestroy(b->ev_stop);
     if (b->own_stream) cudaStreamDestroy(b->own_stream);
     if (prev >= 0) cudaSetDevice(prev);
     delete b;
@@ -755,6 +803,40 @@ int odegpu_batch_sync(odegpu_batch* b) {
 }
 
 int64_t odegpu_batch_launch_count(const odegpu_batch* b) { return b ? b->launches : 0; }
+
+int odegpu_batch_diagnostics(odegpu_batch* b, odegpu_diagnostics* out) {
+    return guarded([&] {
+        check_batch(b);
+        if (!out) throw_invalid("null argument");
+        DeviceGuard g(b->device);
+        CK(cudaMemsetAsync(b->diag, 0, 9 * sizeof(unsigned long long), b->stream));
+        diagnostics_kernel<<<grid_for(b, b->dims.batch_capacity, 256), 256, 0, b->stream>>>(b->a, b->diag);
+        CK(cudaGetLastError());
+        ++b->launches;
+        unsigned long long h[9];
+        CK(cudaMemcpyAsync(h, b->diag, sizeof h, cudaMemcpyDeviceToHost, b->stream));
+        CK(cudaStreamSynchronize(b->stream));
+        out->accepted_steps = static_cast<Index>(h[0]);
+        out->rejected_steps = static_cast<Index>(h[1]);
+        out->event_detections = static_cast<Index>(h[2]);
+        out->secant_failures = static_cast<Index>(h[3]);
+        for (int k = 0; k < 4; ++k) out->reason_counts[k] = static_cast<Index>(h[4 + k]);
+        out->max_trial_steps = static_cast<Index>(h[8]);
+    });
+}
+
+int odegpu_batch_last_kernel_ms(odegpu_batch* b, double* ms) {
+    return guarded([&] {
+        check_batch(b);
+        if (!ms) throw_invalid("null argument");
+        if (!b->timed) throw_invalid("no solve kernel has run on this batch");
+        DeviceGuard g(b->device);
+        CK(cudaEventSynchronize(b->ev_stop));
+        float f = 0;
+        CK(cudaEventElapsedTime(&f, b->ev_start, b->ev_stop));
+        *ms = f;
+    });
+}
 
 int odegpu_dfma_peak(int device, int blocks, int threads, int iters, double* lane_dfma_per_s, double* seconds) {
     return guarded([&] {

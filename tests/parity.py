@@ -81,18 +81,56 @@ def compare(wl, gpu, ref, *, pinned_state=(), pinned_acc=(), time_acc=()) -> dic
             step = np.where(np.isfinite(orf["smallest_step"]), orf["smallest_step"], 0.0)
             dt = np.abs(a_g[c] - a_r[c])
             rep[f"acc{c}_time_steps_off"] = int(np.count_nonzero(same_val & (dt > step * 1.000001 + 1e-15)))
-            rep[f"acc{c}_rel"] = float(np.max(rel_err(a_g[c], a_r[c], atol), initial=0.0))
+            rep[f"acc{c}_time_rel_info"] = float(np.max(rel_err(a_g[c], a_r[c], atol), initial=0.0))
         elif c in pinned_acc:
             rep[f"acc{c}_pinned_abs"] = float(np.max(np.abs(a_g[c] - a_r[c]), initial=0.0))
         else:
             rep[f"acc{c}_rel"] = float(np.max(rel_err(a_g[c], a_r[c], atol), initial=0.0))
             worst = max(worst, rep[f"acc{c}_rel"])
-    rep["td_rel"] = float(np.max(rel_err(gpu["td"], ref["td"], atol), initial=0.0))
-    rep["final_t_rel"] = float(np.max(rel_err(og["final_t"], orf["final_t"], atol), initial=0.0))
+    # Times located by the event machine (final_t of an EventStop, and t0
+    # after BubbleCollapse's finalize) are pinned only by |F| <= tol: two
+    # runs may stop anywhere inside the zone, |dt| <= 2 tol / |dF/dt|.
+    ft_err = rel_err(og["final_t"], orf["final_t"], atol)
+    td_err = rel_err(gpu["td"], ref["td"], atol).reshape(2, n)
+    if ev_tol and stopped.any():
+        slope = event_slope(wl, ref, np.nonzero(stopped)[0])
+        allowed = 4.0 * ev_tol / np.maximum(slope, 1e-300)
+        loc_ok = np.abs(og["final_t"][stopped] - orf["final_t"][stopped]) <= allowed
+        rep["located_t_outside_zone_bound"] = int(np.count_nonzero(~loc_ok))
+        ft_err[stopped] = 0.0
+        td0_ok = np.abs(gpu["td"][:n][stopped] - ref["td"][:n][stopped]) <= allowed
+        rep["located_t_outside_zone_bound"] += int(np.count_nonzero(~td0_ok))
+        td_err[0, stopped] = 0.0
+    rep["td_rel"] = float(np.max(td_err, initial=0.0))
+    rep["final_t_rel"] = float(np.max(ft_err, initial=0.0))
     rep["event_tol"] = ev_tol
     rep["worst_rel"] = worst
     rep["steps"] = int(orf["accepted_steps"].sum() + orf["rejected_steps"].sum())
     return rep
+
+
+def event_slope(wl, ref, idx):
+    """|dF0/dt| at the reference's stop points; F0 = y2 for every stop event
+    of the workloads (duffing.hpp:136, keller_miksis.hpp:324, valve.hpp:435),
+    so dF0/dt = dy2/dt from the model RHS (evaluated by the C oracle)."""
+    import ctypes as C
+
+    from oracle import pyoracle
+
+    lib = pyoracle.load("port")
+    d = wl.model.dims()
+    n = wl.n
+    y = ref["y"].reshape(d.system_dim, n)
+    p = wl.p.reshape(d.param_count, n) if d.param_count else None
+    out = np.empty(idx.size)
+    m = C.byref(wl.model.to_c())
+    for j, i in enumerate(idx):
+        yi = np.ascontiguousarray(y[:, i])
+        pi = np.ascontiguousarray(p[:, i]) if p is not None else np.zeros(1)
+        dy = np.zeros(d.system_dim)
+        lib.odo_rhs(m, float(ref["outcomes"]["final_t"][i]), abi.vptr(yi), abi.vptr(pi), abi.vptr(dy))
+        out[j] = abs(dy[1])
+    return out
 
 
 # Per-config comparison rules (SURVEY.md §8c): which components a stop event
