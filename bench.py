@@ -180,7 +180,7 @@ def run_reference_arm(args, rank, world):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libodref.so not built"}))
         return
     cores = pyoracle.host_cores()
-    sample = args.cpu_sample or {"cfg1": 2048, "cfg2": 65536, "cfg3": 8192, "cfg4": 16384}[args.config]
+    sample = args.cpu_sample or {"cfg1": 46080, "cfg2": 1 << 20, "cfg3": 1 << 17, "cfg4": 1 << 18}[args.config]
     sub = wl.strided(sample)
     td, y, p, acc = sub.arrays()
     oc = None
@@ -206,6 +206,13 @@ def run_reference_arm(args, rank, world):
     }))
 
 
+_T0 = time.time()
+
+
+def log(msg: str):
+    print(f"[bench +{time.time() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -225,6 +232,7 @@ def main():
 
     torch.cuda.set_device(local)
     device = local
+    log(f"torch ready, rank {rank}/{world} on cuda:{local}")
     wl = make_workload(args.config, rank, world)
     n = wl.n
     td, y, p, acc = wl.arrays()
@@ -235,7 +243,9 @@ def main():
     cfg = pkg.SolverConfig(wl.algorithm, wl.dt)
     pkg.linear_set(batch, pool, pkg.LinearCopySpec(0, 0, n))
 
+    log(f"{wl.name}: {n} systems resident")
     peak_lane, _ = pkg.dfma_peak(device)
+    log(f"DFMA peak {peak_lane:.4e} lane-DFMA/s")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{device}")
 
     for _ in range(args.warmup):
@@ -281,6 +291,7 @@ def main():
     achieved = steps_total * wl.instr_per_step / kernel_s  # lane FP64-pipe instr/s (all ranks)
     peak_total = peak_lane * world
 
+    log(f"timed region done: {steps_total} trial steps in {elapsed:.4f} s")
     # ---------------- e2e: through the C ABI with host buffers, per step
     h_td = torch.empty(2 * n, dtype=torch.float64, pin_memory=True).numpy()
     h_y = torch.empty(y.size, dtype=torch.float64, pin_memory=True).numpy()
@@ -327,7 +338,8 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        sample = args.cpu_sample or {"cfg1": 2048, "cfg2": 262144, "cfg3": 16384, "cfg4": 32768}[args.config]
+        sample = args.cpu_sample or {"cfg1": 46080, "cfg2": 1 << 20, "cfg3": 1 << 18, "cfg4": 1 << 19}[args.config]
+        log(f"e2e done ({e2e_value:.4e} steps/s); CPU baseline on {sample} systems")
         cpu = cpu_baseline(wl, sample)
 
     traffic = load_traffic(wl.name)

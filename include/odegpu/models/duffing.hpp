@@ -5,8 +5,10 @@
 
 #include <cmath>
 #include <span>
+#include <stdexcept>
 
 #include "odegpu/hooks.hpp"
+#include "odegpu/system.hpp"
 
 namespace odegpu::models {
 
@@ -120,6 +122,79 @@ struct DuffingLyapunovHooks : HookDefaults {
         y[2] = 1.0;
     }
 };
+
+// ----------------------------------------------------------- host classes
+// Same names, constructors and controls as the reference
+// (duffing.hpp:17-35, 75-180); hooks come from the *Hooks bases above.
+
+/// Parameter slot order [k, B, delta, omega] (duffing.hpp:17-35).
+struct DuffingParams {
+    Real k = 0.2, B = 0.3, delta = 1.0, omega = 1.0;
+    static constexpr Index count = 4;
+    void validate() const {
+        if (!(B > 0) || !(omega > 0)) throw std::invalid_argument("DuffingParams: B and omega must be > 0");
+    }
+    void write(std::span<Real> p) const {
+        p[0] = k;
+        p[1] = B;
+        p[2] = delta;
+        p[3] = omega;
+    }
+};
+
+template <class H, int ID>
+class DuffingFamily : public H {
+public:
+    using hooks_type = H;
+    explicit DuffingFamily(OdeControls ode = OdeControls::uniform(H::kSystemDim, 1e-9, 1e-9))
+        : ode_(std::move(ode)) {}
+    SystemDims dims() const { return dims_of<H>(); }
+    OdeControls ode_controls() const { return ode_; }
+    EventControls event_controls() const { return {}; }
+    odegpu_model descriptor() const { return make_descriptor(ID); }
+
+private:
+    OdeControls ode_;
+};
+
+using DuffingSystem = DuffingFamily<DuffingHooks, ODEGPU_MODEL_DUFFING>;
+using DuffingMaxAccessorySystem = DuffingFamily<DuffingMaxAccessoryHooks, ODEGPU_MODEL_DUFFING_MAX_ACCESSORY>;
+using DuffingMaxMinSystem = DuffingFamily<DuffingMaxMinHooks, ODEGPU_MODEL_DUFFING_MAXMIN>;
+using DuffingLyapunovSystem = DuffingFamily<DuffingLyapunovHooks, ODEGPU_MODEL_DUFFING_LYAPUNOV>;
+
+/// duffing.hpp:122-156
+class DuffingMaxEventSystem : public DuffingMaxEventHooks {
+public:
+    using hooks_type = DuffingMaxEventHooks;
+    explicit DuffingMaxEventSystem(Real event_tolerance = 1e-6, Index stop_after = 0,
+                                   OdeControls ode = OdeControls::uniform(2, 1e-9, 1e-9))
+        : tol_(event_tolerance), stop_(stop_after), ode_(std::move(ode)) {}
+    SystemDims dims() const { return dims_of<hooks_type>(); }
+    OdeControls ode_controls() const { return ode_; }
+    EventControls event_controls() const {
+        return EventControls{.direction = {-1}, .tolerance = {tol_}, .stop_condition = {stop_}};
+    }
+    odegpu_model descriptor() const {
+        return make_descriptor(ODEGPU_MODEL_DUFFING_MAX_EVENT, {tol_, static_cast<double>(stop_)});
+    }
+
+private:
+    Real tol_;
+    Index stop_;
+    OdeControls ode_;
+};
+
+/// duffing.hpp:62-71: lambda = sum(ln sample_n) / (N * period).
+inline Real lyapunov_accumulate(std::span<const Real> samples, Real period) {
+    if (samples.empty()) throw std::invalid_argument("lyapunov_accumulate: no samples");
+    if (!(period > 0)) throw std::invalid_argument("lyapunov_accumulate: period must be > 0");
+    Real sum = 0;
+    for (Real s : samples) {
+        if (!(s > 0)) throw std::invalid_argument("lyapunov_accumulate: nonpositive sample");
+        sum += std::log(s);
+    }
+    return sum / (static_cast<Real>(std::ssize(samples)) * period);
+}
 
 } // namespace odegpu::models
 

@@ -9,8 +9,10 @@
 #include <cmath>
 #include <limits>
 #include <span>
+#include <stdexcept>
 
 #include "odegpu/hooks.hpp"
+#include "odegpu/system.hpp"
 
 namespace odegpu::models {
 
@@ -81,6 +83,90 @@ struct BubbleCollapseHooks : KellerMiksisHooks {
                             std::span<Real>) const {
         time_domain[0] = t;
     }
+};
+
+// ----------------------------------------------------------- host classes
+
+/// Physical description of a dual-frequency driven bubble; defaults are
+/// water with a 10 micron bubble (keller_miksis.hpp:18-32).
+struct BubblePhysical {
+    Real pa1 = 0, pa2 = 0, omega1 = 0, omega2 = 0, theta = 0;
+    Real R_E = 10e-6, c_L = 1497.3, rho_L = 997.1, P_inf = 1.0e5, p_V = 3166.8, sigma = 0.072,
+         mu_L = 8.902e-4, gamma = 1.4;
+};
+
+/// The 13 dimensionless coefficients (keller_miksis.hpp:36-45).
+struct BubbleCoefficients {
+    Real c[13]{};
+    static constexpr Index count = 13;
+    Real operator[](std::size_t i) const { return c[i]; }
+    void write(std::span<Real> p) const {
+        for (std::size_t i = 0; i < 13; ++i) p[i] = c[i];
+    }
+};
+
+/// keller_miksis.hpp:47-77, same operation order (bitwise equal results).
+inline BubbleCoefficients bubble_coefficients(const BubblePhysical& phys) {
+    if (!(phys.omega1 > 0)) throw std::invalid_argument("bubble_coefficients: omega1 must be > 0");
+    if (!(phys.R_E > 0)) throw std::invalid_argument("bubble_coefficients: R_E must be > 0");
+    if (!(phys.gamma > 1)) throw std::invalid_argument("bubble_coefficients: gamma must be > 1");
+    if (!(phys.rho_L > 0) || !(phys.c_L > 0))
+        throw std::invalid_argument("bubble_coefficients: invalid material constants");
+    constexpr Real two_pi = 2.0 * 3.141592653589793238462643383279502884;
+    const Real w = phys.R_E * phys.omega1;
+    const Real S = two_pi / w;
+    const Real G = S * S / phys.rho_L;
+    const Real A = phys.P_inf - phys.p_V;
+    const Real B = 2.0 * phys.sigma / phys.R_E;
+    BubbleCoefficients out;
+    Real* c = out.c;
+    c[0] = (A + B) * G;
+    c[1] = (1.0 - 3.0 * phys.gamma) * (A + B) * S / (phys.rho_L * phys.c_L);
+    c[2] = A * G;
+    c[3] = B * G;
+    c[4] = 4.0 * phys.mu_L / (phys.rho_L * phys.R_E * phys.R_E) * (two_pi / phys.omega1);
+    c[5] = phys.pa1 * G;
+    c[6] = phys.pa2 * G;
+    c[7] = (w / phys.c_L) * c[5];
+    c[8] = (w / phys.c_L) * c[6];
+    c[9] = w / (two_pi * phys.c_L);
+    c[10] = 3.0 * phys.gamma;
+    c[11] = phys.omega2 / phys.omega1;
+    c[12] = phys.theta;
+    return out;
+}
+
+/// keller_miksis.hpp:106-119
+class KellerMiksisSystem : public KellerMiksisHooks {
+public:
+    using hooks_type = KellerMiksisHooks;
+    explicit KellerMiksisSystem(OdeControls ode = OdeControls::uniform(2, 1e-10, 1e-10)) : ode_(std::move(ode)) {}
+    SystemDims dims() const { return dims_of<hooks_type>(); }
+    OdeControls ode_controls() const { return ode_; }
+    EventControls event_controls() const { return {}; }
+    odegpu_model descriptor() const { return make_descriptor(ODEGPU_MODEL_KELLER_MIKSIS); }
+
+private:
+    OdeControls ode_;
+};
+
+/// keller_miksis.hpp:126-165
+class BubbleCollapseSystem : public BubbleCollapseHooks {
+public:
+    using hooks_type = BubbleCollapseHooks;
+    explicit BubbleCollapseSystem(Real event_tolerance = 1e-6,
+                                  OdeControls ode = OdeControls::uniform(2, 1e-10, 1e-10))
+        : tol_(event_tolerance), ode_(std::move(ode)) {}
+    SystemDims dims() const { return dims_of<hooks_type>(); }
+    OdeControls ode_controls() const { return ode_; }
+    EventControls event_controls() const {
+        return EventControls{.direction = {-1}, .tolerance = {tol_}, .stop_condition = {1}};
+    }
+    odegpu_model descriptor() const { return make_descriptor(ODEGPU_MODEL_BUBBLE_COLLAPSE, {tol_}); }
+
+private:
+    Real tol_;
+    OdeControls ode_;
 };
 
 } // namespace odegpu::models

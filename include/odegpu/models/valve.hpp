@@ -5,8 +5,10 @@
 
 #include <cmath>
 #include <span>
+#include <stdexcept>
 
 #include "odegpu/hooks.hpp"
+#include "odegpu/system.hpp"
 
 namespace odegpu::models {
 
@@ -54,6 +56,44 @@ struct ValveHooks : HookDefaults {
         acc[0] = (acc[0] < y[0]) ? y[0] : acc[0];
         acc[1] = (y[0] < acc[1]) ? y[0] : acc[1];
     }
+};
+
+// ----------------------------------------------------------- host classes
+
+/// Parameter slot order [kappa, delta, beta, q, r] (valve.hpp:17-37).
+struct ValveParams {
+    Real kappa = 1.25, delta = 10.0, beta = 20.0, q = 0.3, r = 0.8;
+    static constexpr Index count = 5;
+    void validate() const {
+        if (!(r > 0 && r < 1)) throw std::invalid_argument("ValveParams: r must be in (0, 1)");
+        if (!(q > 0)) throw std::invalid_argument("ValveParams: q must be > 0");
+    }
+    void write(std::span<Real> p) const {
+        p[0] = kappa;
+        p[1] = delta;
+        p[2] = beta;
+        p[3] = q;
+        p[4] = r;
+    }
+};
+
+/// valve.hpp:64-103
+class ValveSystem : public ValveHooks {
+public:
+    using hooks_type = ValveHooks;
+    explicit ValveSystem(Real event_tolerance = 1e-6, OdeControls ode = OdeControls::uniform(3, 1e-10, 1e-10))
+        : tol_(event_tolerance), ode_(std::move(ode)) {}
+    SystemDims dims() const { return dims_of<hooks_type>(); }
+    OdeControls ode_controls() const { return ode_; }
+    EventControls event_controls() const {
+        return EventControls{.direction = {-1, -1}, .tolerance = {tol_, tol_}, .stop_condition = {1, 0},
+                             .max_steps_in_zone = 50};
+    }
+    odegpu_model descriptor() const { return make_descriptor(ODEGPU_MODEL_VALVE, {tol_}); }
+
+private:
+    Real tol_;
+    OdeControls ode_;
 };
 
 } // namespace odegpu::models

@@ -1,0 +1,329 @@
+// test_host_api.cpp — the reference test-suite's batch / driver / scan cases
+// (/root/reference/proj/tests/test_{pool,batch,driver,scan}.cpp) written
+// against the odegpu C++ host API, running on the GPU. Built by `make
+// cpptests` (g++ only; links libodegpu.so) and driven by
+// tests/test_gpu_cpp_api.py. Exit code = number of failed checks.
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <limits>
+#include <numbers>
+#include <string>
+#include <vector>
+
+#include "odegpu/odegpu.hpp"
+
+using namespace odegpu;
+
+static int g_checks = 0, g_failed = 0;
+static const char* g_case = "";
+
+#define CHECK(cond)                                                                              \
+    do {                                                                                         \
+        ++g_checks;                                                                              \
+        if (!(cond)) {                                                                           \
+            ++g_failed;                                                                          \
+            std::printf("FAIL [%s] %s:%d: %s\n", g_case, __FILE__, __LINE__, #cond);             \
+        }                                                                                        \
+    } while (0)
+
+#define CHECK_THROWS_AS(expr, type)                                                              \
+    do {                                                                                         \
+        bool ok_ = false;                                                                        \
+        try {                                                                                    \
+            expr;                                                                                \
+        } catch (const type&) {                                                                  \
+            ok_ = true;                                                                          \
+        } catch (...) {                                                                          \
+        }                                                                                        \
+        CHECK(ok_ && #type);                                                                     \
+    } while (0)
+
+static void run_case(const char* name, const std::function<void()>& f) {
+    g_case = name;
+    try {
+        f();
+    } catch (const std::exception& e) {
+        ++g_failed;
+        std::printf("FAIL [%s] unexpected exception: %s\n", name, e.what());
+    }
+}
+
+constexpr Real kTwoPi = 2.0 * std::numbers::pi_v<Real>;
+
+static ProblemPool duffing_pool(Index n, Real k_lo = 0.2, Real k_hi = 0.3) { // test_batch.cpp:18-33
+    ProblemPool pool(PoolDims{n, 2, 4, 0});
+    for (Index i = 0; i < n; ++i) {
+        pool.time_start(i) = 0.0;
+        pool.time_end(i) = kTwoPi;
+        const Real k = n == 1 ? k_lo : k_lo + (k_hi - k_lo) * static_cast<Real>(i) / static_cast<Real>(n - 1);
+        models::DuffingParams{k, 0.3, 1.0, 1.0}.write(
+            std::span<Real>(std::vector<Real>(4).data(), 4)); // exercise write()
+        pool.param_at(i, 0) = k;
+        pool.param_at(i, 1) = 0.3;
+        pool.param_at(i, 2) = 1.0;
+        pool.param_at(i, 3) = 1.0;
+    }
+    return pool;
+}
+
+int main() {
+    run_case("linear_set round trip and single property", [] { // test_pool.cpp:69-107
+        ProblemPool pool(PoolDims{16, 2, 4, 3});
+        for (Index i = 0; i < 16; ++i) {
+            pool.time_start(i) = 1000 + i;
+            pool.time_end(i) = 2000 + i;
+            for (Index c = 0; c < 2; ++c) pool.state_at(i, c) = 100 * c + i + 0.5;
+            for (Index c = 0; c < 4; ++c) pool.param_at(i, c) = 10000 + 100 * c + i;
+            for (Index c = 0; c < 3; ++c) pool.accessory_at(i, c) = -(100.0 * c + i) - 0.25;
+        }
+        SolverBatch all(BatchDims{16, 2, 4, 0, 3});
+        linear_set(all, pool, {0, 0, 16, CopyMode::All});
+        const SolverBatch& ca = all;
+        for (Index i = 0; i < 16; ++i) {
+            CHECK(ca.time_end(i) == pool.time_end(i));
+            CHECK(ca.state_at(i, 1) == pool.state_at(i, 1));
+            CHECK(ca.param_at(i, 3) == pool.param_at(i, 3));
+            CHECK(ca.accessory_at(i, 2) == pool.accessory_at(i, 2));
+        }
+        SolverBatch part(BatchDims{8, 2, 4, 0, 3});
+        linear_set(part, pool, {2, 5, 4, CopyMode::ActualState});
+        const SolverBatch& cp = part;
+        CHECK(cp.state_at(2, 0) == pool.state_at(5, 0));
+        CHECK(cp.state_at(5, 1) == pool.state_at(8, 1));
+        CHECK(cp.state_at(0, 0) == 0.0 && cp.state_at(6, 0) == 0.0);
+        CHECK(cp.time_end(3) == 0.0 && cp.param_at(3, 0) == 0.0);
+        CHECK_THROWS_AS(linear_set(part, pool, {4, 0, 5, CopyMode::All}), std::out_of_range);
+        CHECK_THROWS_AS(linear_set(part, pool, {0, 12, 5, CopyMode::All}), std::out_of_range);
+        SolverBatch wrong(BatchDims{8, 3, 4, 0, 3});
+        CHECK_THROWS_AS(linear_set(wrong, pool, {0, 0, 2, CopyMode::All}), std::invalid_argument);
+    });
+
+    run_case("host writes through spans reach the device", [] {
+        models::DuffingSystem def;
+        SolverBatch b(make_batch_dims(2, def.dims()));
+        auto td = b.time_domain();
+        td[2] = kTwoPi; // t1 of system 0
+        td[3] = kTwoPi;
+        auto p = b.parameters();
+        for (Index i = 0; i < 2; ++i) {
+            p[static_cast<std::size_t>(0 * 2 + i)] = 0.25;
+            p[static_cast<std::size_t>(1 * 2 + i)] = 0.3;
+            p[static_cast<std::size_t>(2 * 2 + i)] = 1.0;
+            p[static_cast<std::size_t>(3 * 2 + i)] = 1.0;
+        }
+        solve(b, def);
+        const SolverBatch& cb = b;
+        CHECK(cb.outcomes()[0].final_t == kTwoPi);
+        CHECK(cb.outcomes()[1].accepted_steps > 10);
+        CHECK(cb.state_at(0, 0) == cb.state_at(1, 0));
+    });
+
+    run_case("random_set permutation identity", [] { // test_batch.cpp:114-139
+        const Index n = 64;
+        const auto pool = duffing_pool(n);
+        models::DuffingSystem def;
+        SolverBatch plain(make_batch_dims(n, def.dims()));
+        linear_set(plain, pool, {0, 0, n, CopyMode::All});
+        solve(plain, def);
+        std::vector<Index> perm(n), slots(n);
+        for (Index i = 0; i < n; ++i) {
+            perm[static_cast<std::size_t>(i)] = (i * 37 + 11) % n;
+            slots[static_cast<std::size_t>(i)] = i;
+        }
+        SolverBatch permuted(make_batch_dims(n, def.dims()));
+        random_set(permuted, pool, {slots, perm, CopyMode::All});
+        solve(permuted, def);
+        const SolverBatch &cp = permuted, &cq = plain;
+        for (Index i = 0; i < n; ++i) {
+            CHECK(cp.state_at(i, 0) == cq.state_at(perm[static_cast<std::size_t>(i)], 0));
+            CHECK(cp.state_at(i, 1) == cq.state_at(perm[static_cast<std::size_t>(i)], 1));
+        }
+        CHECK_THROWS_AS(random_set(permuted, pool, {{1, 1}, {0, 1}, CopyMode::All}), std::invalid_argument);
+        CHECK_THROWS_AS(random_set(permuted, pool, {{64}, {0}, CopyMode::All}), std::out_of_range);
+    });
+
+    run_case("failure isolation and sticky abort", [] { // test_batch.cpp:139-167
+        const Index n = 32;
+        const auto pool = duffing_pool(n);
+        models::DuffingSystem def;
+        SolverBatch clean(make_batch_dims(n, def.dims()));
+        linear_set(clean, pool, {0, 0, n, CopyMode::All});
+        solve(clean, def);
+        ProblemPool poisoned = pool;
+        poisoned.param_at(7, 1) = std::numeric_limits<Real>::quiet_NaN();
+        SolverBatch dirty(make_batch_dims(n, def.dims()));
+        linear_set(dirty, poisoned, {0, 0, n, CopyMode::All});
+        solve(dirty, def);
+        const SolverBatch &cd = dirty, &cc = clean;
+        CHECK(cd.outcomes()[7].reason == StopReason::NonFiniteAbort);
+        for (Index i = 0; i < n; ++i) {
+            if (i == 7) continue;
+            CHECK(cd.state_at(i, 0) == cc.state_at(i, 0));
+            CHECK(cd.outcomes()[static_cast<std::size_t>(i)].reason == StopReason::ReachedEndTime);
+        }
+        solve(dirty, def);
+        CHECK(cd.outcomes()[7].reason == StopReason::NonFiniteAbort);
+        linear_set(dirty, pool, {7, 7, 1, CopyMode::All});
+        CHECK(cd.outcomes()[7].reason == StopReason::ReachedEndTime);
+    });
+
+    run_case("solve rejects inconsistent setups", [] { // test_batch.cpp:184-204
+        const auto pool = duffing_pool(4);
+        models::DuffingSystem def;
+        SolverBatch batch(make_batch_dims(4, def.dims()));
+        linear_set(batch, pool, {0, 0, 4, CopyMode::All});
+        SolverConfig bad_step;
+        bad_step.initial_time_step = 0.0;
+        CHECK_THROWS_AS(solve(batch, def, bad_step), std::invalid_argument);
+        SolverConfig over_max;
+        over_max.initial_time_step = 1e7;
+        CHECK_THROWS_AS(solve(batch, def, over_max), std::invalid_argument);
+        SolverBatch wrong(BatchDims{4, 3, 4, 0, 0});
+        CHECK_THROWS_AS(solve(wrong, def), std::invalid_argument);
+        auto backwards = duffing_pool(4);
+        backwards.time_end(1) = -1.0;
+        SolverBatch btw(make_batch_dims(4, def.dims()));
+        linear_set(btw, backwards, {0, 0, 4, CopyMode::All});
+        bool msg_ok = false;
+        try {
+            solve(btw, def);
+        } catch (const std::invalid_argument& e) {
+            msg_ok = std::string(e.what()) == "solve: system 1 has t1 < t0";
+        }
+        CHECK(msg_ok);
+    });
+
+    run_case("iterated poincare sampling feeds endpoints forward", [] { // test_driver.cpp:209-234
+        models::DuffingSystem def;
+        const auto pool = duffing_pool(1, 0.215);
+        SolverBatch batch(make_batch_dims(1, def.dims()));
+        linear_set(batch, pool, {0, 0, 1, CopyMode::All});
+        const Index transient = 1024, saved = 32;
+        std::vector<Real> points;
+        solve_iteratively(batch, def, SolverConfig{}, transient + saved, [&](Index iter, const SolverBatch& b) {
+            if (iter >= transient) points.push_back(b.state_at(0, 0));
+        });
+        CHECK(static_cast<Index>(points.size()) == saved);
+        std::vector<Real> centers;
+        for (Real v : points) {
+            bool known = false;
+            for (Real c : centers) known = known || std::abs(v - c) <= 1e-6;
+            if (!known) centers.push_back(v);
+        }
+        CHECK(centers.size() <= 4);
+    });
+
+    run_case("duffing event stop lands on a local maximum", [] { // test_driver.cpp:96-108
+        models::DuffingMaxEventSystem def(1e-6, 1);
+        ProblemPool pool(PoolDims{1, 2, 4, 2});
+        pool.time_end(0) = 1e6;
+        pool.state_at(0, 0) = 0.3;
+        pool.state_at(0, 1) = 0.7;
+        models::DuffingParams{}.write(pool.parameters());
+        SolverBatch b(make_batch_dims(1, def.dims()));
+        linear_set(b, pool, {0, 0, 1, CopyMode::All});
+        solve(b, def);
+        const SolverBatch& cb = b;
+        CHECK(cb.outcomes()[0].reason == StopReason::EventStop);
+        CHECK(std::abs(cb.state_at(0, 1)) <= 1e-6);
+        CHECK(cb.accessory_at(0, 0) == cb.state_at(0, 0));
+    });
+
+    run_case("bubble scan smoke: every iteration stops at a located maximum", [] { // test_scan.cpp:176-196
+        // 1 (pa1) x 1 (pa2) x 2 (f1) x 3 (f2) grid, 8 transient + 4 saved iterations
+        const std::vector<Real> f1 = {20.0, 1000.0}, f2 = {20.0, 141.42135623730951, 1000.0};
+        ProblemPool pool(PoolDims{6, 2, 13, 4});
+        Index i = 0;
+        for (Real a : f1)
+            for (Real b : f2) {
+                models::BubblePhysical phys;
+                phys.pa1 = 1.1e5;
+                phys.pa2 = 0.0;
+                phys.omega1 = a * 1e3 * kTwoPi;
+                phys.omega2 = b * 1e3 * kTwoPi;
+                models::bubble_coefficients(phys).write(
+                    std::span<Real>(std::vector<Real>(13).data(), 13)); // API parity
+                const auto c = models::bubble_coefficients(phys);
+                for (Index k = 0; k < 13; ++k) pool.param_at(i, k) = c[static_cast<std::size_t>(k)];
+                pool.time_end(i) = 1e6;
+                pool.state_at(i, 0) = 1.0;
+                ++i;
+            }
+        models::BubbleCollapseSystem def(1e-6);
+        SolverBatch b(make_batch_dims(6, def.dims()));
+        linear_set(b, pool, {0, 0, 6, CopyMode::All});
+        Index event_stops = 0;
+        std::vector<Real> prev_t0(6, 0.0);
+        bool increasing = true;
+        SolverConfig cfg;
+        solve_iteratively(b, def, cfg, 12, [&](Index, const SolverBatch& bb) {
+            for (Index s = 0; s < 6; ++s) {
+                event_stops += bb.outcomes()[static_cast<std::size_t>(s)].reason == StopReason::EventStop;
+                increasing = increasing && bb.time_start(s) > prev_t0[static_cast<std::size_t>(s)];
+                prev_t0[static_cast<std::size_t>(s)] = bb.time_start(s);
+            }
+        });
+        CHECK(event_stops == 6 * 12);
+        CHECK(increasing);
+    });
+
+    run_case("valve impacts at low flow rate, equilibrium at high", [] { // test_scan.cpp:198-219
+        models::ValveSystem def(1e-6);
+        auto run = [&](Real q, Index transient, Index saved, std::vector<std::pair<Real, Real>>& rows,
+                       Index& equilibria) {
+            ProblemPool pool(PoolDims{1, 3, 5, 2});
+            models::ValveParams{1.25, 10.0, 20.0, q, 0.8}.write(pool.parameters());
+            pool.time_end(0) = 1e6;
+            pool.state_at(0, 0) = 0.2;
+            pool.state_at(0, 2) = 10.2;
+            SolverBatch b(make_batch_dims(1, def.dims()));
+            linear_set(b, pool, {0, 0, 1, CopyMode::All});
+            solve_iteratively(b, def, SolverConfig{}, transient + saved, [&](Index it, const SolverBatch& bb) {
+                equilibria += bb.outcomes()[0].reason == StopReason::EquilibriumStop;
+                if (it >= transient) rows.emplace_back(bb.accessory_at(0, 0), bb.accessory_at(0, 1));
+            });
+        };
+        std::vector<std::pair<Real, Real>> rows;
+        Index eq = 0;
+        run(1.0, 24, 4, rows, eq);
+        CHECK(rows.size() == 4);
+        for (auto [mx, mn] : rows) {
+            CHECK(std::abs(mn) <= 1e-6);
+            CHECK(mx > 0.1);
+        }
+        rows.clear();
+        eq = 0;
+        run(9.0, 256, 8, rows, eq);
+        CHECK(std::abs(rows.back().first - rows.back().second) < 1e-3);
+        CHECK(eq > 0);
+    });
+
+    run_case("lyapunov separates periodic from chaotic damping", [] { // test_scan.cpp:162-174
+        models::DuffingLyapunovSystem def;
+        ProblemPool pool(PoolDims{2, 4, 4, 1});
+        const Real ks[2] = {0.215, 0.24}; // periodic window, chaotic band
+        for (Index i = 0; i < 2; ++i) {
+            pool.time_end(i) = kTwoPi;
+            pool.state_at(i, 2) = 1.0;
+            models::DuffingParams p{ks[i], 0.3, 1.0, 1.0};
+            pool.param_at(i, 0) = p.k;
+            pool.param_at(i, 1) = p.B;
+            pool.param_at(i, 2) = p.delta;
+            pool.param_at(i, 3) = p.omega;
+        }
+        SolverBatch b(make_batch_dims(2, def.dims()));
+        linear_set(b, pool, {0, 0, 2, CopyMode::All});
+        std::vector<std::vector<Real>> samples(2);
+        solve_iteratively(b, def, SolverConfig{}, 256 + 64, [&](Index it, const SolverBatch& bb) {
+            if (it < 256) return;
+            for (Index s = 0; s < 2; ++s) samples[static_cast<std::size_t>(s)].push_back(bb.accessory_at(s, 0));
+            CHECK(bb.state_at(0, 2) == 1.0); // radius reset by finalize
+        });
+        CHECK(models::lyapunov_accumulate(samples[0], kTwoPi) < 0.0);
+        CHECK(models::lyapunov_accumulate(samples[1], kTwoPi) > 0.0);
+    });
+
+    std::printf("%d checks, %d failed\n", g_checks, g_failed);
+    return g_failed;
+}

@@ -139,5 +139,6 @@ RULES = {
     "cfg1_duffing_rk4": dict(time_acc={1: 0, 3: 2}),
     "cfg2_duffing_rkck45_event": dict(time_acc={1: 0}),
     "cfg3_keller_miksis": dict(pinned_state=(1,), time_acc={0: 1, 2: 3}),
-    "cfg4_valve": dict(pinned_state=(1,), time_acc={}),
+    # y1_min sits on the seat (y1 = 0, impact zone |y1| <= tol) for impacting q
+    "cfg4_valve": dict(pinned_state=(1,), pinned_acc=(1,), time_acc={}),
 }
