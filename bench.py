@@ -242,6 +242,14 @@ def main():
     batch.set_stream(stream.cuda_stream)
     cfg = pkg.SolverConfig(wl.algorithm, wl.dt)
     pkg.linear_set(batch, pool, pkg.LinearCopySpec(0, 0, n))
+    # Every step integrates the synthetic batch from its initial conditions:
+    # a pristine copy stays resident in HBM and is restored device-to-device
+    # outside the timed events. (Iterating cfg2 in place is not an option:
+    # from the 3rd forcing period on, 5 of its 2^20 systems enter a
+    # secant/relocation Zeno loop — theta clamps to h*1e-12 forever — in the
+    # reference solver itself.)
+    pristine = pkg.SolverBatch(pkg.make_batch_dims(n, wl.model.dims()), device=device)
+    pkg.batch_copy(pristine, batch)
 
     log(f"{wl.name}: {n} systems resident")
     peak_lane, _ = pkg.dfma_peak(device)
@@ -249,6 +257,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{device}")
 
     for _ in range(args.warmup):
+        pkg.batch_copy(batch, pristine)
         pkg.solve(batch, wl.model, cfg)
 
     # ---------------- timed region (device-resident batch)
@@ -259,6 +268,7 @@ def main():
     ev_ms, kern_ms, steps_total, sys_total, max_trial = [], [], 0, 0, 0
     with ClockSampler(device) as clocks:
         for _ in range(args.steps):
+            pkg.batch_copy(batch, pristine)  # initial conditions, outside the events
             with torch.cuda.stream(stream):
                 flush.fill_(1)  # L2 flush between steps, outside the events
             e0 = torch.cuda.Event(enable_timing=True)
@@ -310,15 +320,12 @@ def main():
     outc = np.zeros(n, dtype=abi.OUTCOME_DTYPE)
     if world > 1:
         torch.distributed.barrier()
+    # the chunked pool pipeline: 4 chunks, H2D of chunk k+1 and D2H of chunk
+    # k-1 overlap chunk k's kernels (odegpu_solve_pool)
+    cap = max(1, n // 4)
     for _ in range(args.e2e_steps):
         t0 = time.perf_counter()
-        pkg.linear_set(batch, pin_pool, pkg.LinearCopySpec(0, 0, n))
-        pkg.solve(batch, wl.model, cfg)
-        pkg.api.check(lib.odegpu_batch_read(batch.handle, abi.PROP_STATE, abi.dptr(o_y)))
-        pkg.api.check(lib.odegpu_batch_read(batch.handle, abi.PROP_TIME_DOMAIN, abi.dptr(o_td)))
-        if acc.size:
-            pkg.api.check(lib.odegpu_batch_read(batch.handle, abi.PROP_ACCESSORIES, abi.dptr(o_a)))
-        pkg.api.check(lib.odegpu_batch_read_outcomes(batch.handle, abi.vptr(outc)))
+        o_td, o_y, o_a, outc = pkg.solve_pool(pin_pool, wl.model, cfg, cap, 1, devices=(device,))
         e2e_s += time.perf_counter() - t0
         e2e_steps += int(outc["accepted_steps"].sum() + outc["rejected_steps"].sum())
     if world > 1:
@@ -389,7 +396,9 @@ def main():
             "hbm_gbs": hbm_bytes / per_launch_s / 1e9,
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "steps": args.e2e_steps, "path": "linear_set (pinned H2D) + solve + D2H of td/state/acc/outcomes"},
+                "steps": args.e2e_steps,
+                "path": "odegpu_solve_pool over the pinned host pool: 4 chunks, double-buffered H2D / solve / "
+                        "D2H of td, state, accessories and outcomes into host arrays, wall-clock"},
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
     }

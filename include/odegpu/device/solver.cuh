@@ -56,7 +56,8 @@ struct BatchArrays {
     Index* detections;
     Index* secant_failures;
     Real* smallest_step;
-    Index n;
+    Index n;                  // stride (batch capacity)
+    Index count;              // systems [0, count) are integrated (count <= n)
     unsigned long long* work; // next system to hand out (zeroed before launch)
 };
 
@@ -80,8 +81,10 @@ __device__ __forceinline__ Real smax(Real a, Real b) { return (a < b) ? b : a; }
 __device__ __forceinline__ Real smin(Real a, Real b) { return (b < a) ? b : a; }
 __device__ __forceinline__ Real sclamp(Real v, Real lo, Real hi) { return (v < lo) ? lo : (hi < v) ? hi : v; }
 
-template <int N>
-using Vec = Real[N];
+/// Compiler-level memory fence: nothing cached from shared memory survives
+/// it in registers (keeps cold state and shared-memory parameters out of the
+/// register file across the RK stages).
+__device__ __forceinline__ void cold_fence() { asm volatile("" ::: "memory"); }
 
 template <class H>
 __device__ __forceinline__ void rhs(const H& m, Real t, const Real (&y)[H::kSystemDim],
@@ -93,24 +96,56 @@ __device__ __forceinline__ void rhs(const H& m, Real t, const Real (&y)[H::kSyst
 /// One trial step from (t, y) with step h (steppers.hpp:82-139). Writes the
 /// proposed state, the embedded error |y5 - y4| (RKCK45) and whether
 /// anything is non-finite.
+/// The stages are a rolled loop around ONE inlined RHS call site: a uniform
+/// switch on the stage index forms the stage argument from the tableau row
+/// and stores the stage derivative, so the (large) RHS — libdevice pow /
+/// sincos for Keller-Miksis — is emitted once instead of 4-6 times and the
+/// step loop fits the instruction cache. Every lane of a warp runs the same
+/// stage, so the switch never diverges. Expressions are those of the
+/// reference, operation for operation.
 template <class H, Algorithm ALG>
 __device__ __forceinline__ bool rk_step(const H& m, Real t, Real h, const Real (&y)[H::kSystemDim],
                                         const Real* p, Real (&out)[H::kSystemDim],
                                         Real (&err)[H::kSystemDim]) {
     constexpr int N = H::kSystemDim;
-    Real k1[N], k2[N], k3[N], k4[N], yt[N];
+    Real k1[N], k2[N], k3[N], k4[N], k5[N], k6[N];
     bool finite = true;
     if constexpr (ALG == Algorithm::RK4) {
-        rhs(m, t, y, p, k1);
+#pragma unroll 1
+        for (int s = 0; s < 4; ++s) {
+            cold_fence();
+            Real ts, yt[N], kk[N];
+            switch (s) {
+            case 0:
+                ts = t;
 #pragma unroll
-        for (int i = 0; i < N; ++i) yt[i] = y[i] + 0.5 * h * k1[i];
-        rhs(m, t + 0.5 * h, yt, p, k2);
+                for (int i = 0; i < N; ++i) yt[i] = y[i];
+                break;
+            case 1:
+                ts = t + 0.5 * h;
 #pragma unroll
-        for (int i = 0; i < N; ++i) yt[i] = y[i] + 0.5 * h * k2[i];
-        rhs(m, t + 0.5 * h, yt, p, k3);
+                for (int i = 0; i < N; ++i) yt[i] = y[i] + 0.5 * h * k1[i];
+                break;
+            case 2:
+                ts = t + 0.5 * h;
 #pragma unroll
-        for (int i = 0; i < N; ++i) yt[i] = y[i] + h * k3[i];
-        rhs(m, t + h, yt, p, k4);
+                for (int i = 0; i < N; ++i) yt[i] = y[i] + 0.5 * h * k2[i];
+                break;
+            default:
+                ts = t + h;
+#pragma unroll
+                for (int i = 0; i < N; ++i) yt[i] = y[i] + h * k3[i];
+                break;
+            }
+            rhs(m, ts, yt, p, kk);
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                if (s == 0) k1[i] = kk[i];
+                else if (s == 1) k2[i] = kk[i];
+                else if (s == 2) k3[i] = kk[i];
+                else k4[i] = kk[i];
+            }
+        }
 #pragma unroll
         for (int i = 0; i < N; ++i) {
             out[i] = y[i] + (h / 6.0) * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
@@ -118,26 +153,57 @@ __device__ __forceinline__ bool rk_step(const H& m, Real t, Real h, const Real (
             finite = finite && isfinite(out[i]);
         }
     } else {
-        Real k5[N], k6[N];
-        rhs(m, t, y, p, k1);
+#pragma unroll 1
+        for (int s = 0; s < 6; ++s) {
+            cold_fence();
+            Real ts, yt[N], kk[N];
+            switch (s) {
+            case 0:
+                ts = t;
 #pragma unroll
-        for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a21 * k1[i]);
-        rhs(m, t + ck::c2 * h, yt, p, k2);
+                for (int i = 0; i < N; ++i) yt[i] = y[i];
+                break;
+            case 1:
+                ts = t + ck::c2 * h;
 #pragma unroll
-        for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a31 * k1[i] + ck::a32 * k2[i]);
-        rhs(m, t + ck::c3 * h, yt, p, k3);
+                for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a21 * k1[i]);
+                break;
+            case 2:
+                ts = t + ck::c3 * h;
 #pragma unroll
-        for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a41 * k1[i] + ck::a42 * k2[i] + ck::a43 * k3[i]);
-        rhs(m, t + ck::c4 * h, yt, p, k4);
+                for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a31 * k1[i] + ck::a32 * k2[i]);
+                break;
+            case 3:
+                ts = t + ck::c4 * h;
 #pragma unroll
-        for (int i = 0; i < N; ++i)
-            yt[i] = y[i] + h * (ck::a51 * k1[i] + ck::a52 * k2[i] + ck::a53 * k3[i] + ck::a54 * k4[i]);
-        rhs(m, t + ck::c5 * h, yt, p, k5);
+                for (int i = 0; i < N; ++i)
+                    yt[i] = y[i] + h * (ck::a41 * k1[i] + ck::a42 * k2[i] + ck::a43 * k3[i]);
+                break;
+            case 4:
+                ts = t + ck::c5 * h;
 #pragma unroll
-        for (int i = 0; i < N; ++i)
-            yt[i] = y[i] + h * (ck::a61 * k1[i] + ck::a62 * k2[i] + ck::a63 * k3[i] + ck::a64 * k4[i] +
-                                ck::a65 * k5[i]);
-        rhs(m, t + ck::c6 * h, yt, p, k6);
+                for (int i = 0; i < N; ++i)
+                    yt[i] = y[i] + h * (ck::a51 * k1[i] + ck::a52 * k2[i] + ck::a53 * k3[i] + ck::a54 * k4[i]);
+                break;
+            default:
+                ts = t + ck::c6 * h;
+#pragma unroll
+                for (int i = 0; i < N; ++i)
+                    yt[i] = y[i] + h * (ck::a61 * k1[i] + ck::a62 * k2[i] + ck::a63 * k3[i] + ck::a64 * k4[i] +
+                                        ck::a65 * k5[i]);
+                break;
+            }
+            rhs(m, ts, yt, p, kk);
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                if (s == 0) k1[i] = kk[i];
+                else if (s == 1) k2[i] = kk[i];
+                else if (s == 2) k3[i] = kk[i];
+                else if (s == 3) k4[i] = kk[i];
+                else if (s == 4) k5[i] = kk[i];
+                else k6[i] = kk[i];
+            }
+        }
 #pragma unroll
         for (int i = 0; i < N; ++i) {
             out[i] = y[i] + h * (ck::b1 * k1[i] + ck::b3 * k3[i] + ck::b4 * k4[i] + ck::b6 * k6[i]);
@@ -184,57 +250,100 @@ __device__ __forceinline__ Index fetch_system(unsigned long long* work) {
     return static_cast<Index>(base + g.thread_rank());
 }
 
+
 enum Phase : int { kFetch = 0, kStep = 1, kSecant = 2, kCommit = 3, kFinish = 4, kDone = 5 };
 
 constexpr int kMaxSecantIterations = 50; // events.hpp:190
 
-/// The ensemble kernel. One instantiation per (model, algorithm): hooks are
-/// inlined, widths are compile-time, all per-system state is in registers.
-template <class H, Algorithm ALG>
+/// Cold per-lane state of the state machine: everything that is not needed
+/// inside the Runge-Kutta stages. It lives in shared memory as structure of
+/// arrays (one column per thread, bank-conflict free) so that only the hot
+/// set — t, h, y and the stage vectors — occupies registers during the
+/// stages; that is what sets occupancy (SURVEY.md §8d register table).
+template <class H, int BLOCK>
+struct ColdState {
+    static constexpr int N = H::kSystemDim;
+    static constexpr int E = H::kEventCount > 0 ? H::kEventCount : 1;
+    static constexpr int A = H::kAccessoryCount > 0 ? H::kAccessoryCount : 1;
+    Real td[2][BLOCK];
+    Real acc[A][BLOCK];
+    Real y_land[N][BLOCK];
+    Real f_land[E][BLOCK];
+    Real prev_value[E][BLOCK]; // EventMachine (events.hpp:76-178)
+    Real t1[BLOCK], h[BLOCK], h_try[BLOCK], h_next[BLOCK], t_land[BLOCK], smallest[BLOCK];
+    Real th_prev[BLOCK], f_prev[BLOCK], th_cur[BLOCK], f_cur[BLOCK], th_min[BLOCK], b_th[BLOCK], b_f[BLOCK];
+    long long sys[BLOCK];
+    unsigned n_acc[BLOCK], n_rej[BLOCK], n_det[BLOCK], n_secf[BLOCK];
+    int counter[E][BLOCK];
+    int steps_in_zone[BLOCK], s_it[BLOCK], s_idx[BLOCK], located[BLOCK];
+    unsigned char leaving[E][BLOCK], clipped[BLOCK], relocated[BLOCK], s_conv[BLOCK], reason[BLOCK];
+};
+
+/// Parameters with >= 5 slots live in shared memory (one row of odd stride
+/// per thread: conflict-free 8-byte loads), smaller sets in registers.
+template <class H>
+struct ParamPolicy {
+    static constexpr int NP = H::kParamCount;
+    static constexpr bool kShared = NP >= 5;
+    static constexpr int kStride = kShared ? (NP | 1) : 1;
+    static constexpr int kRegs = kShared ? 1 : (NP > 0 ? NP : 1);
+};
+
+/// The ensemble loop. One instantiation per (model, algorithm): hooks are
+/// inlined, widths are compile-time; hot state in registers, cold state in
+/// shared memory.
+template <class H, Algorithm ALG, int BLOCK>
 __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, const Controls& c) {
     constexpr int N = H::kSystemDim;
-    constexpr int P = H::kParamCount > 0 ? H::kParamCount : 1;
-    constexpr int E = H::kEventCount;
-    constexpr int EE = E > 0 ? E : 1;
-    constexpr int A = H::kAccessoryCount > 0 ? H::kAccessoryCount : 1;
-    constexpr int NP = H::kParamCount, NA = H::kAccessoryCount;
+    constexpr int NP = H::kParamCount, NA = H::kAccessoryCount, E = H::kEventCount;
+    constexpr int EE = E > 0 ? E : 1, A = NA > 0 ? NA : 1;
+    using PP = ParamPolicy<H>;
     static_assert(N <= kMaxDim && E <= kMaxEvents, "model wider than the device controls");
+
+    __shared__ ColdState<H, BLOCK> cs;
+    __shared__ Real sp[PP::kShared ? BLOCK * PP::kStride : 1];
+    const int tid = threadIdx.x;
     const Index n = b.n;
-
-    // ---- per-lane registers
-    Index sys = -1;
-    Real td[2], y[N], p[P], acc[A];
-    Real t = 0, t1 = 0, h = 0;
-    // event machine (events.hpp:76-178)
-    Real prev_value[EE];
-    Index counter[EE];
-    bool leaving[EE];
-    Index steps_in_zone = 0;
-    // outcome (driver.hpp:34-42)
-    Index n_acc = 0, n_rej = 0, n_det = 0, n_secf = 0;
-    Real smallest = 0;
-    std::uint8_t reason = 0;
-    // the step in flight
-    Real h_try = 0, h_next = 0, h_step = 0, t_land = 0;
-    bool clipped = false, relocated = false;
-    int located = -1;
-    Real y_land[N], f_land[EE];
-    // secant (events.hpp:200-241)
-    int s_idx = 0, s_it = 0;
-    bool s_conv = false;
-    Real th_prev = 0, f_prev = 0, th_cur = 0, f_cur = 0, th_min = 0, b_th = 0, b_f = 0;
-
-    int phase = kFetch;
+    Real preg[PP::kRegs];
+    Real* const prow = PP::kShared ? sp + tid * PP::kStride : preg;
 
     const auto S = [](Real* a, int len) { return std::span<Real>(a, static_cast<std::size_t>(len)); };
     const auto CS = [](const Real* a, int len) { return std::span<const Real>(a, static_cast<std::size_t>(len)); };
+#define ODEGPU_C(field) cs.field[tid]
 
+    // ---- hot registers
+    Real t = 0, h_step = 0;
+    Real y[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) y[i] = 0;
+    int phase = kFetch;
+
+    // Helpers moving the small hook arguments between shared memory and
+    // register arrays around (infrequent) hook calls.
+    const auto load_acc = [&](Real (&a)[A]) {
+#pragma unroll
+        for (int i = 0; i < A; ++i) a[i] = ODEGPU_C(acc[i]);
+    };
+    const auto store_acc = [&](const Real (&a)[A]) {
+#pragma unroll
+        for (int i = 0; i < NA; ++i) ODEGPU_C(acc[i]) = a[i];
+    };
+    const auto landed_values = [&](Real tt) { // F at the landed point -> f_land
+        Real yl[N], f[EE];
+#pragma unroll
+        for (int i = 0; i < N; ++i) yl[i] = ODEGPU_C(y_land[i]);
+        m.event_values(tt, CS(yl, N), CS(prow, NP), S(f, E));
+#pragma unroll
+        for (int i = 0; i < E; ++i) ODEGPU_C(f_land[i]) = f[i];
+    };
     // Ends a secant location (driver.hpp:157-164).
     const auto end_secant = [&]() {
-        if (!s_conv) ++n_secf;
-        relocated = b_th < h_try;
-        t_land = (clipped && !relocated) ? t1 : t + b_th;
-        m.event_values(t_land, CS(y_land, N), CS(p, NP), S(f_land, E));
+        if (!ODEGPU_C(s_conv)) ++ODEGPU_C(n_secf);
+        const bool rel = ODEGPU_C(b_th) < ODEGPU_C(h_try);
+        ODEGPU_C(relocated) = rel;
+        const Real tl = (ODEGPU_C(clipped) && !rel) ? ODEGPU_C(t1) : t + ODEGPU_C(b_th);
+        ODEGPU_C(t_land) = tl;
+        landed_values(tl);
         phase = kCommit;
     };
 
@@ -242,137 +351,151 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
         // ================= PREPARE: bring this lane to a pending RK evaluation
         for (;;) {
             if (phase == kFetch) {
-                sys = fetch_system(b.work);
-                if (sys >= n) {
+                const Index sys = fetch_system(b.work);
+                if (sys >= b.count) {
                     phase = kDone;
                     break;
                 }
                 if (b.reason[sys] == static_cast<std::uint8_t>(StopReason::NonFiniteAbort)) continue; // solve.hpp:98
-                td[0] = b.td[sys];
-                td[1] = b.td[sys + n];
+                ODEGPU_C(sys) = sys;
+                Real td[2] = {b.td[sys], b.td[sys + n]};
 #pragma unroll
                 for (int i = 0; i < N; ++i) y[i] = b.state[sys + i * n];
 #pragma unroll
-                for (int i = 0; i < H::kParamCount; ++i) p[i] = __ldg(b.params + sys + i * n);
+                for (int i = 0; i < NP; ++i) prow[i] = __ldg(b.params + sys + i * n);
+                Real acc[A];
 #pragma unroll
-                for (int i = 0; i < H::kAccessoryCount; ++i) acc[i] = b.acc[sys + i * n];
-                n_acc = n_rej = n_det = n_secf = 0;
-                smallest = __longlong_as_double(0x7ff0000000000000LL); // +inf
-                reason = static_cast<std::uint8_t>(StopReason::ReachedEndTime);
+                for (int i = 0; i < NA; ++i) acc[i] = b.acc[sys + i * n];
+                ODEGPU_C(n_acc) = ODEGPU_C(n_rej) = ODEGPU_C(n_det) = ODEGPU_C(n_secf) = 0u;
+                ODEGPU_C(smallest) = __longlong_as_double(0x7ff0000000000000LL); // +inf
+                ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::ReachedEndTime);
                 // driver.hpp:96-107
-                m.initialize(td[0], S(td, 2), S(y, N), CS(p, NP), S(acc, NA));
+                m.initialize(td[0], S(td, 2), S(y, N), CS(prow, NP), S(acc, NA));
+                ODEGPU_C(td[0]) = td[0];
+                ODEGPU_C(td[1]) = td[1];
+                store_acc(acc);
                 t = td[0];
-                t1 = td[1];
+                ODEGPU_C(t1) = td[1];
                 if constexpr (E > 0) {
                     Real f0[EE];
-                    m.event_values(t, CS(y, N), CS(p, NP), S(f0, E));
+                    m.event_values(t, CS(y, N), CS(prow, NP), S(f0, E));
 #pragma unroll
                     for (int i = 0; i < E; ++i) {
-                        prev_value[i] = f0[i];
-                        leaving[i] = zone_of(f0[i], c.tolerance[i]) == kZoneInside;
-                        counter[i] = 0;
+                        ODEGPU_C(prev_value[i]) = f0[i];
+                        ODEGPU_C(leaving[i]) = zone_of(f0[i], c.tolerance[i]) == kZoneInside;
+                        ODEGPU_C(counter[i]) = 0;
                     }
-                    steps_in_zone = 0;
+                    ODEGPU_C(steps_in_zone) = 0;
                 }
-                h = ALG == Algorithm::RK4 ? c.initial_time_step
-                                         : sclamp(c.initial_time_step, c.min_step, c.max_step);
+                ODEGPU_C(h) = ALG == Algorithm::RK4 ? c.initial_time_step
+                                                    : sclamp(c.initial_time_step, c.min_step, c.max_step);
                 phase = kStep;
             }
             if (phase == kCommit) {
                 // driver.hpp:170-227
-                if (t_land <= t) {
-                    reason = static_cast<std::uint8_t>(StopReason::NonFiniteAbort);
+                const Real tl = ODEGPU_C(t_land);
+                if (tl <= t) {
+                    ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::NonFiniteAbort);
                     phase = kFinish;
                 } else {
-                    const Real advanced = t_land - t;
+                    const Real advanced = tl - t;
 #pragma unroll
-                    for (int i = 0; i < N; ++i) y[i] = y_land[i];
-                    t = t_land;
-                    ++n_acc;
-                    smallest = smin(smallest, advanced);
+                    for (int i = 0; i < N; ++i) y[i] = ODEGPU_C(y_land[i]);
+                    t = tl;
+                    ++ODEGPU_C(n_acc);
+                    ODEGPU_C(smallest) = smin(ODEGPU_C(smallest), advanced);
                     bool event_stop = false;
+                    Real acc[A];
+                    load_acc(acc);
                     if constexpr (E > 0) {
+                        const int located = ODEGPU_C(located);
                         bool det[EE];
+                        int cnt[EE];
 #pragma unroll
                         for (int i = 0; i < E; ++i) { // EventMachine::commit, events.hpp:134-156
-                            const int pz = zone_of(prev_value[i], c.tolerance[i]);
-                            const int nz = zone_of(f_land[i], c.tolerance[i]);
-                            const bool kind = pz != kZoneNone && nz != kZoneNone && !leaving[i] &&
+                            const Real fl = ODEGPU_C(f_land[i]);
+                            const int pz = zone_of(ODEGPU_C(prev_value[i]), c.tolerance[i]);
+                            const int nz = zone_of(fl, c.tolerance[i]);
+                            const bool kind = pz != kZoneNone && nz != kZoneNone && !ODEGPU_C(leaving[i]) &&
                                               classify(pz, nz, c.direction[i]) != kKindNone;
                             det[i] = kind || i == located;
-                            if (det[i]) {
-                                ++counter[i];
-                                ++n_det;
-                            }
+                            cnt[i] = ODEGPU_C(counter[i]) + (det[i] ? 1 : 0);
+                            ODEGPU_C(counter[i]) = cnt[i];
+                            if (det[i]) ++ODEGPU_C(n_det);
                         }
                         Real f_post[EE];
                         if (located >= 0) {
 #pragma unroll
                             for (int i = 0; i < E; ++i)
-                                if (i == located) m.event_action(i, counter[i], t, S(y, N), CS(p, NP));
-                            m.event_values(t, CS(y, N), CS(p, NP), S(f_post, E));
+                                if (i == located) m.event_action(i, cnt[i], t, S(y, N), CS(prow, NP));
+                            m.event_values(t, CS(y, N), CS(prow, NP), S(f_post, E));
                         } else {
 #pragma unroll
-                            for (int i = 0; i < E; ++i) f_post[i] = f_land[i];
+                            for (int i = 0; i < E; ++i) f_post[i] = ODEGPU_C(f_land[i]);
                         }
                         bool any_inside = false; // EventMachine::refresh, events.hpp:160-173
 #pragma unroll
                         for (int i = 0; i < E; ++i) {
                             const int z = zone_of(f_post[i], c.tolerance[i]);
                             if (z == kZoneNone) continue;
-                            prev_value[i] = f_post[i];
-                            leaving[i] = z == kZoneInside;
+                            ODEGPU_C(prev_value[i]) = f_post[i];
+                            ODEGPU_C(leaving[i]) = z == kZoneInside;
                             any_inside = any_inside || z == kZoneInside;
                         }
-                        steps_in_zone = any_inside ? steps_in_zone + 1 : 0;
+                        ODEGPU_C(steps_in_zone) = any_inside ? ODEGPU_C(steps_in_zone) + 1 : 0;
 #pragma unroll
                         for (int i = 0; i < E; ++i)
-                            if (det[i]) m.event_accessory(i, counter[i], t, CS(y, N), CS(p, NP), S(acc, NA));
+                            if (det[i]) m.event_accessory(i, cnt[i], t, CS(y, N), CS(prow, NP), S(acc, NA));
 #pragma unroll
                         for (int i = 0; i < E; ++i)
-                            if (det[i] && c.stop_condition[i] != 0 && counter[i] >= c.stop_condition[i])
-                                event_stop = true;
+                            if (det[i] && c.stop_condition[i] != 0 && cnt[i] >= c.stop_condition[i]) event_stop = true;
                     }
-                    m.ordinary_accessory(t, CS(y, N), CS(p, NP), S(acc, NA));
+                    m.ordinary_accessory(t, CS(y, N), CS(prow, NP), S(acc, NA));
+                    store_acc(acc);
                     if (event_stop) {
-                        reason = static_cast<std::uint8_t>(StopReason::EventStop);
+                        ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::EventStop);
                         phase = kFinish;
-                    } else if (E > 0 && steps_in_zone >= c.max_steps_in_zone) {
-                        reason = static_cast<std::uint8_t>(StopReason::EquilibriumStop);
+                    } else if (E > 0 && ODEGPU_C(steps_in_zone) >= c.max_steps_in_zone) {
+                        ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::EquilibriumStop);
                         phase = kFinish;
                     } else {
-                        if (ALG == Algorithm::RKCK45 && !relocated) h = h_next;
+                        if (ALG == Algorithm::RKCK45 && !ODEGPU_C(relocated)) ODEGPU_C(h) = ODEGPU_C(h_next);
                         phase = kStep;
                     }
                 }
             }
             if (phase == kFinish) {
                 // driver.hpp:231-233, then scatter_system (batch.cpp:32-40)
-                m.finalize(t, S(td, 2), S(y, N), CS(p, NP), S(acc, NA));
+                Real td[2] = {ODEGPU_C(td[0]), ODEGPU_C(td[1])};
+                Real acc[A];
+                load_acc(acc);
+                m.finalize(t, S(td, 2), S(y, N), CS(prow, NP), S(acc, NA));
+                const Index sys = ODEGPU_C(sys);
                 b.td[sys] = td[0];
                 b.td[sys + n] = td[1];
 #pragma unroll
                 for (int i = 0; i < N; ++i) b.state[sys + i * n] = y[i];
 #pragma unroll
-                for (int i = 0; i < H::kAccessoryCount; ++i) b.acc[sys + i * n] = acc[i];
+                for (int i = 0; i < NA; ++i) b.acc[sys + i * n] = acc[i];
                 b.final_t[sys] = t;
-                b.reason[sys] = reason;
-                b.accepted[sys] = n_acc;
-                b.rejected[sys] = n_rej;
-                b.detections[sys] = n_det;
-                b.secant_failures[sys] = n_secf;
-                b.smallest_step[sys] = smallest;
+                b.reason[sys] = ODEGPU_C(reason);
+                b.accepted[sys] = ODEGPU_C(n_acc);
+                b.rejected[sys] = ODEGPU_C(n_rej);
+                b.detections[sys] = ODEGPU_C(n_det);
+                b.secant_failures[sys] = ODEGPU_C(n_secf);
+                b.smallest_step[sys] = ODEGPU_C(smallest);
                 phase = kFetch;
                 continue;
             }
             if (phase == kStep) {
                 // driver.hpp:109-119
+                const Real t1 = ODEGPU_C(t1);
                 if (!(t < t1)) {
                     phase = kFinish;
                     continue;
                 }
-                h_try = h;
-                clipped = false;
+                Real h_try = ODEGPU_C(h);
+                bool clipped = false;
                 if (t + h_try >= t1) {
                     h_try = t1 - t;
                     clipped = true;
@@ -382,26 +505,29 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     phase = kFinish;
                     continue;
                 }
+                ODEGPU_C(h_try) = h_try;
+                ODEGPU_C(clipped) = clipped;
                 h_step = h_try;
                 break;
             }
             if (phase == kSecant) {
                 // events.hpp:214-219: the pre-step exits of one secant iteration
-                if (s_it > kMaxSecantIterations) {
+                if (ODEGPU_C(s_it) > kMaxSecantIterations) {
                     end_secant();
                     continue;
                 }
-                const Real denom = f_cur - f_prev;
+                const Real th_cur = ODEGPU_C(th_cur), f_cur = ODEGPU_C(f_cur);
+                const Real denom = f_cur - ODEGPU_C(f_prev);
                 if (denom == 0) {
                     end_secant();
                     continue;
                 }
-                Real theta = th_cur - f_cur * (th_cur - th_prev) / denom;
+                Real theta = th_cur - f_cur * (th_cur - ODEGPU_C(th_prev)) / denom;
                 if (!isfinite(theta)) {
                     end_secant();
                     continue;
                 }
-                theta = sclamp(theta, th_min, h_try);
+                theta = sclamp(theta, ODEGPU_C(th_min), ODEGPU_C(h_try));
                 if (theta == th_cur) {
                     end_secant();
                     continue;
@@ -413,18 +539,22 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
         if (phase == kDone) break;
 
         // ================= the shared Runge-Kutta evaluation
+        cold_fence();
         Real yn[N], err[N];
-        const bool nonfinite = rk_step<H, ALG>(m, t, h_step, y, p, yn, err);
+        const bool nonfinite = rk_step<H, ALG>(m, t, h_step, y, prow, yn, err);
+        cold_fence();
 
         // ================= ABSORB
         if (phase == kStep) {
+            const Real h_try = h_step;
+            Real h_next;
             if constexpr (ALG == Algorithm::RK4) {
                 if (nonfinite) { // driver.hpp:124-128
-                    reason = static_cast<std::uint8_t>(StopReason::NonFiniteAbort);
+                    ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::NonFiniteAbort);
                     phase = kFinish;
                     continue;
                 }
-                h_next = h;
+                h_next = ODEGPU_C(h);
             } else {
                 // error_ratio (steppers.hpp:154-163) + control_step (176-198)
                 Real ratio = 0.0;
@@ -436,7 +566,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 bool accepted;
                 if (nonfinite) {
                     if (h_try <= c.min_step) {
-                        reason = static_cast<std::uint8_t>(StopReason::NonFiniteAbort);
+                        ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::NonFiniteAbort);
                         phase = kFinish;
                         continue;
                     }
@@ -453,28 +583,33 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     }
                 }
                 if (!accepted) {
-                    ++n_rej;
-                    h = h_next;
+                    ++ODEGPU_C(n_rej);
+                    ODEGPU_C(h) = h_next;
                     continue;
                 }
             }
+            ODEGPU_C(h_next) = h_next;
             // accepted: driver.hpp:146-168
-            t_land = clipped ? t1 : t + h_try;
+            const Real tl = ODEGPU_C(clipped) ? ODEGPU_C(t1) : t + h_try;
+            ODEGPU_C(t_land) = tl;
 #pragma unroll
-            for (int i = 0; i < N; ++i) y_land[i] = yn[i];
-            located = -1;
-            relocated = false;
+            for (int i = 0; i < N; ++i) ODEGPU_C(y_land[i]) = yn[i];
+            int located = -1;
+            ODEGPU_C(relocated) = false;
             phase = kCommit;
             if constexpr (E > 0) {
-                m.event_values(t_land, CS(y_land, N), CS(p, NP), S(f_land, E));
+                Real f[EE];
+                m.event_values(tl, CS(yn, N), CS(prow, NP), S(f, E));
+#pragma unroll
+                for (int i = 0; i < E; ++i) ODEGPU_C(f_land[i]) = f[i];
                 // EventMachine::peek (events.hpp:111-125): highest index wins
                 bool needs = false;
 #pragma unroll
                 for (int i = E - 1; i >= 0; --i) {
                     if (located >= 0) break;
-                    const int pz = zone_of(prev_value[i], c.tolerance[i]);
-                    const int nz = zone_of(f_land[i], c.tolerance[i]);
-                    if (pz == kZoneNone || nz == kZoneNone || leaving[i]) continue;
+                    const int pz = zone_of(ODEGPU_C(prev_value[i]), c.tolerance[i]);
+                    const int nz = zone_of(f[i], c.tolerance[i]);
+                    if (pz == kZoneNone || nz == kZoneNone || ODEGPU_C(leaving[i])) continue;
                     const int kind = classify(pz, nz, c.direction[i]);
                     if (kind != kKindNone) {
                         located = i;
@@ -483,27 +618,32 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 }
                 if (located >= 0 && needs) {
                     // start locate_secant (events.hpp:207-212); y_land holds y(h)
-                    s_idx = located;
-                    s_it = 1;
-                    s_conv = false;
-                    th_prev = 0;
-                    th_cur = h_try;
-                    th_min = h_try * 1e-12;
+                    ODEGPU_C(s_idx) = located;
+                    ODEGPU_C(s_it) = 1;
+                    ODEGPU_C(s_conv) = false;
+                    ODEGPU_C(th_prev) = 0;
+                    ODEGPU_C(th_cur) = h_try;
+                    ODEGPU_C(th_min) = h_try * 1e-12;
+                    Real fp = 0, fc = 0;
 #pragma unroll
                     for (int i = 0; i < E; ++i)
-                        if (i == s_idx) {
-                            f_prev = prev_value[i];
-                            f_cur = f_land[i];
+                        if (i == located) {
+                            fp = ODEGPU_C(prev_value[i]);
+                            fc = f[i];
                         }
-                    b_th = h_try;
-                    b_f = f_cur;
+                    ODEGPU_C(f_prev) = fp;
+                    ODEGPU_C(f_cur) = fc;
+                    ODEGPU_C(b_th) = h_try;
+                    ODEGPU_C(b_f) = fc;
                     phase = kSecant;
                 }
             }
+            ODEGPU_C(located) = located;
         } else { // kSecant: one secant iteration's step is in (events.hpp:222-240)
             if constexpr (E > 0) {
                 Real fs[EE];
-                m.event_values(t + h_step, CS(yn, N), CS(p, NP), S(fs, E));
+                m.event_values(t + h_step, CS(yn, N), CS(prow, NP), S(fs, E));
+                const int s_idx = ODEGPU_C(s_idx);
                 Real f = fs[0];
                 Real tol = c.tolerance[0];
 #pragma unroll
@@ -516,30 +656,31 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     end_secant();
                     continue;
                 }
-                if (fabs(f) < fabs(b_f)) {
-                    b_th = h_step;
-                    b_f = f;
+                if (fabs(f) < fabs(ODEGPU_C(b_f))) {
+                    ODEGPU_C(b_th) = h_step;
+                    ODEGPU_C(b_f) = f;
 #pragma unroll
-                    for (int i = 0; i < N; ++i) y_land[i] = yn[i];
+                    for (int i = 0; i < N; ++i) ODEGPU_C(y_land[i]) = yn[i];
                 }
                 if (fabs(f) <= tol) {
-                    s_conv = true;
+                    ODEGPU_C(s_conv) = true;
                     end_secant();
                     continue;
                 }
-                th_prev = th_cur;
-                f_prev = f_cur;
-                th_cur = h_step;
-                f_cur = f;
-                ++s_it;
+                ODEGPU_C(th_prev) = ODEGPU_C(th_cur);
+                ODEGPU_C(f_prev) = ODEGPU_C(f_cur);
+                ODEGPU_C(th_cur) = h_step;
+                ODEGPU_C(f_cur) = f;
+                ++ODEGPU_C(s_it);
             }
         }
     }
+#undef ODEGPU_C
 }
 
 template <class H, Algorithm ALG, int BLOCK, int MIN_BLOCKS>
 __global__ void __launch_bounds__(BLOCK, MIN_BLOCKS) solve_kernel(H model, BatchArrays b, Controls c) {
-    solve_lanes<H, ALG>(model, b, c);
+    solve_lanes<H, ALG, BLOCK>(model, b, c);
 }
 
 } // namespace odegpu::device

@@ -532,7 +532,19 @@ static void integrate_system(const Model* m, int alg, double dt, const odegpu_od
     }
     double h = alg == ODEGPU_RK4 ? dt : sclamp(dt, ode->min_step, ode->max_step);
 
+    /* Debug aid only (unset = reference behaviour): abandon a system after
+     * ODO_DEBUG_MAX_STEPS trial steps and report it on stderr. */
+    static long long debug_cap = -2;
+    if (debug_cap == -2) {
+        const char* e = getenv("ODO_DEBUG_MAX_STEPS");
+        debug_cap = e ? atoll(e) : -1;
+    }
     while (t < t1) {
+        if (debug_cap > 0 && oc->accepted_steps + oc->rejected_steps > debug_cap) {
+            fprintf(stderr, "odo: step cap hit at t=%.17g h=%.17g y=(%.17g, %.17g) p0=%.17g p1=%.17g\n", t, h,
+                    state[0], m->n > 1 ? state[1] : 0.0, m->np ? p[0] : 0.0, m->np > 1 ? p[1] : 0.0);
+            break;
+        }
         double h_try = h;
         int clipped = 0;
         if (t + h_try >= t1) {

@@ -24,4 +24,7 @@ from .api import (  # noqa: F401
     random_set,
     solve,
     solve_iteratively,
+    batch_copy,
+    slice_range,
+    solve_pool,
 )

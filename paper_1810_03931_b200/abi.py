@@ -153,7 +153,26 @@ class Diagnostics(C.Structure):
     ]
 
 
+class ChunkRecord(C.Structure):
+    _fields_ = [
+        ("td", C.POINTER(C.c_double)),
+        ("state", C.POINTER(C.c_double)),
+        ("accessories", C.POINTER(C.c_double)),
+        ("outcomes", C.c_void_p),
+    ]
+
+
+class PoolOut(C.Structure):
+    _fields_ = [
+        ("time_domain", C.POINTER(C.c_double)),
+        ("state", C.POINTER(C.c_double)),
+        ("accessories", C.POINTER(C.c_double)),
+        ("outcomes", C.c_void_p),
+    ]
+
+
 SINK = C.CFUNCTYPE(C.c_int, Index, C.c_void_p, C.c_void_p)
+CHUNK_SINK = C.CFUNCTYPE(C.c_int, Index, Index, Index, C.POINTER(ChunkRecord), C.c_void_p)
 
 
 def dptr(a: np.ndarray | None):
@@ -214,6 +233,20 @@ def _bind(lib):
         "odegpu_batch_diagnostics": (C.c_int, [vp, P(Diagnostics)]),
         "odegpu_batch_last_kernel_ms": (C.c_int, [vp, P(C.c_double)]),
         "odegpu_dfma_peak": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, P(C.c_double), P(C.c_double)]),
+        "odegpu_batch_copy": (C.c_int, [vp, vp]),
+        "odegpu_solve_pool": (
+            C.c_int,
+            [P(PoolView), P(PoolOut), P(Model), P(SolverConfig), P(OdeControls), P(EventControls), Index, Index,
+             Index, C.c_uint32, CHUNK_SINK, vp, C.c_int],
+        ),
+        "odegpu_solve_pool_multi": (
+            C.c_int,
+            [P(PoolView), P(PoolOut), P(Model), P(SolverConfig), P(OdeControls), P(EventControls), Index, Index,
+             Index, C.c_uint32, CHUNK_SINK, vp, P(C.c_int), C.c_int],
+        ),
+        "odegpu_slice": (C.c_int, [Index, C.c_int, C.c_int, P(Index), P(Index)]),
+        "odegpu_host_register": (C.c_int, [vp, C.c_size_t]),
+        "odegpu_host_unregister": (C.c_int, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -383,6 +383,80 @@ def solve_iteratively(batch: SolverBatch, defn: SystemDef, cfg: SolverConfig | N
     check(rc)
 
 
+def batch_copy(dst: SolverBatch, src: SolverBatch):
+    """Device-to-device copy of every array and outcome (same dims)."""
+    check(dst._lib.odegpu_batch_copy(dst.handle, src.handle))
+
+
+def slice_range(total: int, parts: int, index: int) -> tuple[int, int]:
+    """Contiguous [begin, end) owned by part `index` of `parts` (odegpu_slice)."""
+    b, e = C.c_int64(), C.c_int64()
+    check(abi.load().odegpu_slice(total, parts, index, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+RECORD_TD, RECORD_STATE, RECORD_ACC, RECORD_OUTCOMES = 1, 2, 8, 16
+
+
+def solve_pool(pool: ProblemPool, defn: SystemDef, cfg: SolverConfig | None, batch_capacity: int, iterations: int,
+               *, record_from: int | None = None, record_mask: int = 0, on_chunk=None, write_back: bool = True,
+               devices=(0,)):
+    """Chunked pool pipeline (odegpu_solve_pool[_multi]): the pool runs through
+    the device(s) in chunks of `batch_capacity`, `iterations` solves each,
+    with double-buffered copies. Returns (td, state, acc, outcomes) endpoint
+    arrays (pool layout) if `write_back`. `on_chunk(start, count, records)`
+    receives, per chunk, a dict of recorded per-iteration arrays."""
+    cfg = cfg or SolverConfig()
+    ode, ev = _controls(defn)
+    d = defn.dims()
+    n = pool.size()
+    record_from = iterations if record_from is None else record_from
+    n_rec = iterations - record_from
+    out_arrays = None
+    out = None
+    if write_back:
+        out_arrays = (np.zeros(2 * n), np.zeros(d.system_dim * n), np.zeros(d.accessory_count * n),
+                      np.zeros(n, dtype=abi.OUTCOME_DTYPE))
+        out = abi.PoolOut(abi.dptr(out_arrays[0]), abi.dptr(out_arrays[1]),
+                          abi.dptr(out_arrays[2] if d.accessory_count else None), abi.vptr(out_arrays[3]))
+    err = []
+
+    def _sink(start, count, nrec, rec_p, _u):
+        try:
+            rec = rec_p.contents
+            got = {}
+            if record_mask & RECORD_TD:
+                got["td"] = np.ctypeslib.as_array(rec.td, shape=(nrec * 2 * count,)).copy()
+            if record_mask & RECORD_STATE:
+                got["state"] = np.ctypeslib.as_array(rec.state, shape=(nrec * d.system_dim * count,)).copy()
+            if record_mask & RECORD_ACC and d.accessory_count:
+                got["acc"] = np.ctypeslib.as_array(rec.accessories, shape=(nrec * d.accessory_count * count,)).copy()
+            if record_mask & RECORD_OUTCOMES:
+                buf = (C.c_char * (nrec * count * abi.OUTCOME_DTYPE.itemsize)).from_address(rec.outcomes)
+                got["outcomes"] = np.frombuffer(buf, dtype=abi.OUTCOME_DTYPE).copy()
+            on_chunk(int(start), int(count), got)
+            return 0
+        except BaseException as e:
+            err.append(e)
+            return 1
+
+    cb = abi.CHUNK_SINK(_sink) if on_chunk else abi.CHUNK_SINK()
+    lib = abi.load()
+    args = (C.byref(pool.view()), C.byref(out) if out is not None else None, C.byref(defn.to_c()),
+            C.byref(cfg.to_c()), C.byref(ode), C.byref(ev), batch_capacity, iterations, record_from,
+            record_mask if on_chunk else 0, cb, None)
+    devices = list(devices)
+    if len(devices) == 1:
+        rc = lib.odegpu_solve_pool(*args, devices[0])
+    else:
+        dev_arr = (C.c_int * len(devices))(*devices)
+        rc = lib.odegpu_solve_pool_multi(*args, dev_arr, len(devices))
+    if err:
+        raise err[0]
+    check(rc)
+    return out_arrays
+
+
 def dfma_peak(device: int = 0, blocks: int | None = None, threads: int = 256, iters: int = 4096):
     """Lane-DFMA/s of the FP64 pipe measured by the microbenchmark kernel."""
     lib = abi.load()

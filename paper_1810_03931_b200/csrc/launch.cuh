@@ -1,0 +1,68 @@
+// launch.cuh — instantiation and launch of the per-model solve kernels.
+// Included by the model translation units (models_*.cu) only.
+#pragma once
+
+#include "internal.cuh"
+
+namespace odegpu::detail {
+
+// The skip flag: when the time-domain check found a bad system the solve
+// kernel must not touch anything (the reference throws before solving,
+// solve.hpp:159-161).
+template <class H, Algorithm ALG, int BLOCK, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
+    guarded_solve_kernel(H model, dev::BatchArrays b, dev::Controls c, const unsigned long long* first_bad) {
+    if (*first_bad != ~0ull) return;
+    dev::solve_lanes<H, ALG, BLOCK>(model, b, c);
+}
+
+/// Per-model launch policy: resident blocks of kBlock threads per SM that
+/// __launch_bounds__ asks ptxas for (register cap 65536 / (kMinBlocks *
+/// kBlock)). Chosen per model family from ncu runs;
+/// ODEGPU_MIN_BLOCKS overrides it for tuning builds.
+template <class H>
+struct LaunchPolicy {
+#ifdef ODEGPU_MIN_BLOCKS
+    static constexpr int kMinBlocks = ODEGPU_MIN_BLOCKS;
+#else
+    static constexpr int kMinBlocks = 4;
+#endif
+};
+
+template <class H, Algorithm ALG>
+void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
+    constexpr int kMin = LaunchPolicy<H>::kMinBlocks;
+    auto kern = guarded_solve_kernel<H, ALG, kBlock, kMin>;
+    static int resident = -1; // per instantiation: resident blocks per SM
+    if (resident < 0) {
+        int r = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kern, kBlock, 0));
+        resident = std::max(r, 1);
+    }
+    const Index n = b->a.count;
+    const Index persistent = Index(b->num_sms) * resident;
+    const Index needed = (n + kBlock - 1) / kBlock;
+    const int grid = static_cast<int>(std::max<Index>(1, std::min(needed, persistent)));
+    CK(cudaMemsetAsync(b->a.work, 0, sizeof(unsigned long long), b->stream));
+    CK(cudaEventRecord(b->ev_start, b->stream));
+    kern<<<grid, kBlock, 0, b->stream>>>(hooks, b->a, c, b->first_bad);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(b->ev_stop, b->stream));
+    b->timed = true;
+    ++b->launches;
+}
+
+template <class H>
+void launch_alg(odegpu_batch* b, const H& hooks, int algorithm, const dev::Controls& c) {
+    if (algorithm == ODEGPU_RK4)
+        launch_one<H, Algorithm::RK4>(b, hooks, c);
+    else
+        launch_one<H, Algorithm::RKCK45>(b, hooks, c);
+}
+
+template <class H>
+void set_dims(odegpu_system_dims* d) {
+    *d = odegpu_system_dims{H::kSystemDim, H::kParamCount, H::kEventCount, H::kAccessoryCount};
+}
+
+} // namespace odegpu::detail

@@ -1,0 +1,52 @@
+// models_fakes.cu — solve-kernel instantiations of the reference test-suite
+// fakes (test_fakes.cuh), so its known answers run through the product path.
+#include "launch.cuh"
+#include "test_fakes.cuh"
+
+namespace odegpu::detail {
+
+bool family_dims_fakes(const odegpu_model& m, odegpu_system_dims* d) {
+    switch (m.id) {
+    case ODEGPU_MODEL_CONSTANT: set_dims<fakes::ConstantHooks>(d); return true;
+    case ODEGPU_MODEL_CUBIC_TIME: set_dims<fakes::CubicTimeHooks>(d); return true;
+    case ODEGPU_MODEL_EXPONENTIAL: set_dims<fakes::ExponentialHooks>(d); return true;
+    case ODEGPU_MODEL_UNIT_SLOPE: set_dims<fakes::UnitSlopeHooks>(d); return true;
+    case ODEGPU_MODEL_COUNTING: set_dims<fakes::CountingHooks>(d); return true;
+    case ODEGPU_MODEL_RAMP: set_dims<fakes::RampHooks>(d); return true;
+    case ODEGPU_MODEL_DECAY: set_dims<fakes::DecayHooks>(d); return true;
+    case ODEGPU_MODEL_SEAT_CONTACT: set_dims<fakes::SeatContactHooks>(d); return true;
+    case ODEGPU_MODEL_HARMONIC: set_dims<fakes::HarmonicHooks>(d); return true;
+    case ODEGPU_MODEL_BLOWUP: set_dims<fakes::BlowUpHooks>(d); return true;
+    default: return false;
+    }
+}
+
+bool family_launch_fakes(odegpu_batch* b, const odegpu_model& m, int alg, const dev::Controls& c) {
+    const double* k = m.consts;
+    switch (m.id) {
+    case ODEGPU_MODEL_CONSTANT: {
+        fakes::ConstantHooks h;
+        h.value = k[0];
+        launch_alg(b, h, alg, c);
+        return true;
+    }
+    case ODEGPU_MODEL_CUBIC_TIME: launch_alg(b, fakes::CubicTimeHooks{}, alg, c); return true;
+    case ODEGPU_MODEL_EXPONENTIAL: launch_alg(b, fakes::ExponentialHooks{}, alg, c); return true;
+    case ODEGPU_MODEL_UNIT_SLOPE: launch_alg(b, fakes::UnitSlopeHooks{}, alg, c); return true;
+    case ODEGPU_MODEL_COUNTING: launch_alg(b, fakes::CountingHooks{}, alg, c); return true;
+    case ODEGPU_MODEL_RAMP: {
+        fakes::RampHooks h;
+        h.slope = k[0];
+        h.level = k[1];
+        launch_alg(b, h, alg, c);
+        return true;
+    }
+    case ODEGPU_MODEL_DECAY: launch_alg(b, fakes::DecayHooks{}, alg, c); return true;
+    case ODEGPU_MODEL_SEAT_CONTACT: launch_alg(b, fakes::SeatContactHooks{}, alg, c); return true;
+    case ODEGPU_MODEL_HARMONIC: launch_alg(b, fakes::HarmonicHooks{}, alg, c); return true;
+    case ODEGPU_MODEL_BLOWUP: launch_alg(b, fakes::BlowUpHooks{}, alg, c); return true;
+    default: return false;
+    }
+}
+
+} // namespace odegpu::detail
