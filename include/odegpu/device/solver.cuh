@@ -103,17 +103,68 @@ __device__ __forceinline__ void rhs(const H& m, Real t, const Real (&y)[H::kSyst
 /// step loop fits the instruction cache. Every lane of a warp runs the same
 /// stage, so the switch never diverges. Expressions are those of the
 /// reference, operation for operation.
-template <class H, Algorithm ALG>
+template <class H, Algorithm ALG, bool ROLLED, bool FENCE>
 __device__ __forceinline__ bool rk_step(const H& m, Real t, Real h, const Real (&y)[H::kSystemDim],
                                         const Real* p, Real (&out)[H::kSystemDim],
                                         Real (&err)[H::kSystemDim]) {
     constexpr int N = H::kSystemDim;
     Real k1[N], k2[N], k3[N], k4[N], k5[N], k6[N];
     bool finite = true;
+    if constexpr (!ROLLED) {
+        // Straight-line stages: best when the RHS is small (Duffing, valve):
+        // no stage dispatch, the scheduler sees across stage boundaries.
+        Real yt[N];
+        if constexpr (ALG == Algorithm::RK4) {
+            rhs(m, t, y, p, k1);
+#pragma unroll
+            for (int i = 0; i < N; ++i) yt[i] = y[i] + 0.5 * h * k1[i];
+            rhs(m, t + 0.5 * h, yt, p, k2);
+#pragma unroll
+            for (int i = 0; i < N; ++i) yt[i] = y[i] + 0.5 * h * k2[i];
+            rhs(m, t + 0.5 * h, yt, p, k3);
+#pragma unroll
+            for (int i = 0; i < N; ++i) yt[i] = y[i] + h * k3[i];
+            rhs(m, t + h, yt, p, k4);
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                out[i] = y[i] + (h / 6.0) * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
+                err[i] = 0.0;
+                finite = finite && isfinite(out[i]);
+            }
+        } else {
+            rhs(m, t, y, p, k1);
+#pragma unroll
+            for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a21 * k1[i]);
+            rhs(m, t + ck::c2 * h, yt, p, k2);
+#pragma unroll
+            for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a31 * k1[i] + ck::a32 * k2[i]);
+            rhs(m, t + ck::c3 * h, yt, p, k3);
+#pragma unroll
+            for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a41 * k1[i] + ck::a42 * k2[i] + ck::a43 * k3[i]);
+            rhs(m, t + ck::c4 * h, yt, p, k4);
+#pragma unroll
+            for (int i = 0; i < N; ++i)
+                yt[i] = y[i] + h * (ck::a51 * k1[i] + ck::a52 * k2[i] + ck::a53 * k3[i] + ck::a54 * k4[i]);
+            rhs(m, t + ck::c5 * h, yt, p, k5);
+#pragma unroll
+            for (int i = 0; i < N; ++i)
+                yt[i] = y[i] + h * (ck::a61 * k1[i] + ck::a62 * k2[i] + ck::a63 * k3[i] + ck::a64 * k4[i] +
+                                    ck::a65 * k5[i]);
+            rhs(m, t + ck::c6 * h, yt, p, k6);
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                out[i] = y[i] + h * (ck::b1 * k1[i] + ck::b3 * k3[i] + ck::b4 * k4[i] + ck::b6 * k6[i]);
+                err[i] = fabs(h * (ck::d1 * k1[i] + ck::d3 * k3[i] + ck::d4 * k4[i] + ck::d5 * k5[i] +
+                                   ck::d6 * k6[i]));
+                finite = finite && isfinite(out[i]) && isfinite(err[i]);
+            }
+        }
+        return !finite;
+    }
     if constexpr (ALG == Algorithm::RK4) {
 #pragma unroll 1
         for (int s = 0; s < 4; ++s) {
-            cold_fence();
+            if constexpr (FENCE) cold_fence();
             Real ts, yt[N], kk[N];
             switch (s) {
             case 0:
@@ -155,7 +206,7 @@ __device__ __forceinline__ bool rk_step(const H& m, Real t, Real h, const Real (
     } else {
 #pragma unroll 1
         for (int s = 0; s < 6; ++s) {
-            cold_fence();
+            if constexpr (FENCE) cold_fence();
             Real ts, yt[N], kk[N];
             switch (s) {
             case 0:
@@ -279,14 +330,41 @@ struct ColdState {
     unsigned char leaving[E][BLOCK], clipped[BLOCK], relocated[BLOCK], s_conv[BLOCK], reason[BLOCK];
 };
 
-/// Parameters with >= 5 slots live in shared memory (one row of odd stride
-/// per thread: conflict-free 8-byte loads), smaller sets in registers.
+/// Per-model kernel structure, chosen from ncu measurements
+/// and specialisable for custom models:
+///  * kRolledStages   — one RHS call site in a rolled stage loop (pays off
+///                      when the RHS is large: I-cache, registers);
+///  * kColdInShared   — cold lane state in shared memory instead of registers;
+///  * kParamsInShared — per-system parameters in shared memory (one row of
+///                      odd stride per thread, conflict-free 8-byte loads).
+/// ODEGPU_POLICY_{ROLLED,COLD_SHARED,PARAMS_SHARED} override every model in
+/// tuning builds (scripts/build_variants.sh).
 template <class H>
-struct ParamPolicy {
-    static constexpr int NP = H::kParamCount;
-    static constexpr bool kShared = NP >= 5;
-    static constexpr int kStride = kShared ? (NP | 1) : 1;
-    static constexpr int kRegs = kShared ? 1 : (NP > 0 ? NP : 1);
+struct KernelPolicy {
+    static constexpr bool kRolledStages = false;
+    static constexpr bool kColdInShared = true;
+    static constexpr bool kParamsInShared = H::kParamCount >= 5;
+};
+
+template <class H>
+struct EffectivePolicy {
+#ifdef ODEGPU_POLICY_ROLLED
+    static constexpr bool kRolledStages = ODEGPU_POLICY_ROLLED;
+#else
+    static constexpr bool kRolledStages = KernelPolicy<H>::kRolledStages;
+#endif
+#ifdef ODEGPU_POLICY_COLD_SHARED
+    static constexpr bool kColdInShared = ODEGPU_POLICY_COLD_SHARED;
+#else
+    static constexpr bool kColdInShared = KernelPolicy<H>::kColdInShared;
+#endif
+#ifdef ODEGPU_POLICY_PARAMS_SHARED
+    static constexpr bool kParamsInShared = ODEGPU_POLICY_PARAMS_SHARED && H::kParamCount > 0;
+#else
+    static constexpr bool kParamsInShared = KernelPolicy<H>::kParamsInShared && H::kParamCount > 0;
+#endif
+    static constexpr int kParamStride = kParamsInShared ? (H::kParamCount | 1) : 1;
+    static constexpr int kParamRegs = kParamsInShared ? 1 : (H::kParamCount > 0 ? H::kParamCount : 1);
 };
 
 /// The ensemble loop. One instantiation per (model, algorithm): hooks are
@@ -297,15 +375,22 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
     constexpr int N = H::kSystemDim;
     constexpr int NP = H::kParamCount, NA = H::kAccessoryCount, E = H::kEventCount;
     constexpr int EE = E > 0 ? E : 1, A = NA > 0 ? NA : 1;
-    using PP = ParamPolicy<H>;
+    using Pol = EffectivePolicy<H>;
     static_assert(N <= kMaxDim && E <= kMaxEvents, "model wider than the device controls");
+    constexpr bool kFence = Pol::kColdInShared || Pol::kParamsInShared;
 
-    __shared__ ColdState<H, BLOCK> cs;
-    __shared__ Real sp[PP::kShared ? BLOCK * PP::kStride : 1];
-    const int tid = threadIdx.x;
+    // cold state: a shared-memory column per thread, or a register record
+    __shared__ ColdState<H, Pol::kColdInShared ? BLOCK : 1> cs_shared;
+    ColdState<H, 1> cs_regs;
+    auto& cs = [&]() -> auto& {
+        if constexpr (Pol::kColdInShared) return cs_shared;
+        else return cs_regs;
+    }();
+    const int tid = Pol::kColdInShared ? static_cast<int>(threadIdx.x) : 0;
+    __shared__ Real sp[Pol::kParamsInShared ? BLOCK * Pol::kParamStride : 1];
     const Index n = b.n;
-    Real preg[PP::kRegs];
-    Real* const prow = PP::kShared ? sp + tid * PP::kStride : preg;
+    Real preg[Pol::kParamRegs];
+    Real* const prow = Pol::kParamsInShared ? sp + threadIdx.x * Pol::kParamStride : preg;
 
     const auto S = [](Real* a, int len) { return std::span<Real>(a, static_cast<std::size_t>(len)); };
     const auto CS = [](const Real* a, int len) { return std::span<const Real>(a, static_cast<std::size_t>(len)); };
@@ -539,10 +624,10 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
         if (phase == kDone) break;
 
         // ================= the shared Runge-Kutta evaluation
-        cold_fence();
+        if constexpr (kFence) cold_fence();
         Real yn[N], err[N];
-        const bool nonfinite = rk_step<H, ALG>(m, t, h_step, y, prow, yn, err);
-        cold_fence();
+        const bool nonfinite = rk_step<H, ALG, Pol::kRolledStages, Pol::kParamsInShared>(m, t, h_step, y, prow, yn, err);
+        if constexpr (kFence) cold_fence();
 
         // ================= ABSORB
         if (phase == kStep) {

@@ -1,16 +1,20 @@
 #!/bin/bash
-# Tuning builds: libodegpu with a forced __launch_bounds__ min-blocks value,
-# into paper_1810_03931_b200/lib/variants/libodegpu_mb<N>.so (load with ODEGPU_LIB=...).
+# Tuning builds of libodegpu with forced kernel-structure policies:
+#   scripts/build_variants.sh name:ROLLED:COLD_SHARED:PARAMS_SHARED:MIN_BLOCKS ...
+# -> paper_1810_03931_b200/lib/variants/libodegpu_<name>.so (load with ODEGPU_LIB=...)
 set -e
 cd "$(dirname "$0")/.."
 NVFLAGS="-std=c++20 --expt-relaxed-constexpr -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -Xcompiler -fPIC -Iinclude -Ipaper_1810_03931_b200/csrc"
-mkdir -p paper_1810_03931_b200/lib/variants
-for mb in "$@"; do
-  od=build/var_mb$mb; mkdir -p $od
+mkdir -p paper_1810_03931_b200/lib/variants build/variants
+for spec in "$@"; do
+  IFS=: read name rolled cold params mb <<< "$spec"
+  od=build/variants/$name; mkdir -p $od
+  defs="-DODEGPU_POLICY_ROLLED=$rolled -DODEGPU_POLICY_COLD_SHARED=$cold -DODEGPU_POLICY_PARAMS_SHARED=$params -DODEGPU_MIN_BLOCKS=$mb"
   for f in paper_1810_03931_b200/csrc/*.cu; do
     b=$(basename $f .cu)
-    nvcc $NVFLAGS -DODEGPU_MIN_BLOCKS=$mb -c -o $od/$b.o $f &
+    nvcc $NVFLAGS $defs -Xptxas -v -c -o $od/$b.o $f 2> $od/$b.ptxas &
   done
   wait
-  nvcc -gencode arch=compute_100a,code=sm_100a -shared -Xcompiler -fPIC -o paper_1810_03931_b200/lib/variants/libodegpu_mb$mb.so $od/*.o
+  cat $od/*.ptxas > $od/ptxas.txt
+  nvcc -gencode arch=compute_100a,code=sm_100a -shared -Xcompiler -fPIC -o paper_1810_03931_b200/lib/variants/libodegpu_$name.so $od/*.o
 done
