@@ -343,7 +343,7 @@ template <class H>
 struct KernelPolicy {
     static constexpr bool kRolledStages = false;
     static constexpr bool kColdInShared = true;
-    static constexpr bool kParamsInShared = H::kParamCount >= 5;
+    static constexpr bool kParamsInShared = false;
 };
 
 template <class H>

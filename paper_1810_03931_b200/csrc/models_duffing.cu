@@ -3,9 +3,38 @@
 #include "launch.cuh"
 #include "odegpu/models/duffing.hpp"
 
+namespace odegpu::device {
+template <>
+struct KernelPolicy<odegpu::models::DuffingMaxMinHooks> {
+    static constexpr bool kRolledStages = false, kColdInShared = false, kParamsInShared = false;
+};
+} // namespace odegpu::device
+
 namespace odegpu::detail {
 
-// 4-dim Lyapunov system: 156 registers unbounded; 3 blocks/SM (<= 168 regs) keeps it spill-free.
+// Policies from the variant sweep (profiles/r01_variants.md):
+// * cfg1 (RK4 + max/min accessories, only 46 080 systems = 2.4 blocks/SM):
+//   occupancy is not the limit, so all state stays in registers (0.615 ms vs
+//   0.72 ms with the cold state in shared memory).
+// * the event / accessory RKCK45 models: cold state in shared memory frees
+//   enough registers (123 -> 72) for 7 blocks of 128 threads per SM.
+template <>
+struct LaunchPolicy<models::DuffingMaxMinHooks> {
+    static constexpr int kMinBlocks = 1;
+};
+template <>
+struct LaunchPolicy<models::DuffingMaxEventHooks> {
+    static constexpr int kMinBlocks = 7;
+};
+template <>
+struct LaunchPolicy<models::DuffingMaxAccessoryHooks> {
+    static constexpr int kMinBlocks = 7;
+};
+template <>
+struct LaunchPolicy<models::DuffingHooks> {
+    static constexpr int kMinBlocks = 7;
+};
+// 4-dim Lyapunov system: 3 blocks/SM (<= 168 regs) keeps it spill-free.
 template <>
 struct LaunchPolicy<models::DuffingLyapunovHooks> {
     static constexpr int kMinBlocks = 3;

@@ -5,6 +5,14 @@
 
 namespace odegpu::detail {
 
+// Valve: small RHS, straight-line stages, cold state in shared memory,
+// 7 blocks/SM (72 registers; profiles/r01_variants.md: 3.49 ms vs 4.72 ms
+// all-register).
+template <>
+struct LaunchPolicy<models::ValveHooks> {
+    static constexpr int kMinBlocks = 7;
+};
+
 bool family_dims_valve(const odegpu_model& m, odegpu_system_dims* d) {
     if (m.id != ODEGPU_MODEL_VALVE) return false;
     set_dims<models::ValveHooks>(d);
