@@ -22,6 +22,7 @@
 #include <cstdint>
 #include <span>
 
+#include "odegpu/device/dmath.cuh"
 #include "odegpu/hooks.hpp"
 
 namespace odegpu::device {
@@ -659,7 +660,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     h_next = smax(h_try * c.step_shrink_limit, c.min_step);
                 } else {
                     accepted = ratio <= 1.0;
-                    Real factor = 0.9 * pow(ratio, -0.2);
+                    Real factor = 0.9 * dmath::pow(ratio, -0.2);
                     factor = sclamp(factor, c.step_shrink_limit, c.step_grow_limit);
                     h_next = sclamp(h_try * factor, c.min_step, c.max_step);
                     if (!accepted && h_try <= c.min_step) {

@@ -13,6 +13,9 @@
 
 #include "odegpu/hooks.hpp"
 #include "odegpu/system.hpp"
+#if defined(__CUDACC__)
+#include "odegpu/device/dmath.cuh"
+#endif
 
 namespace odegpu::models {
 
@@ -33,15 +36,20 @@ ODEGPU_HD ODEGPU_INLINE void keller_miksis_rhs(Real tau, std::span<const Real> y
     const Real arg2 = two_pi * c[11] * tau + c[12];
     Real s1, c1, s2, c2;
 #if defined(__CUDA_ARCH__)
-    sincos(arg1, &s1, &c1);
-    sincos(arg2, &s2, &c2);
+    device::dmath::sincos(arg1, &s1, &c1);
+    device::dmath::sincos(arg2, &s2, &c2);
 #else
     s1 = std::sin(arg1);
     c1 = std::cos(arg1);
     s2 = std::sin(arg2);
     c2 = std::cos(arg2);
 #endif
-    const Real numerator = (c[0] + c[1] * y2) * pow(1.0 / y1, c[10]) - c[2] * (1.0 + c[9] * y2) - c[3] / y1 -
+#if defined(__CUDA_ARCH__)
+    const Real pw = device::dmath::pow(1.0 / y1, c[10]);
+#else
+    const Real pw = std::pow(1.0 / y1, c[10]);
+#endif
+    const Real numerator = (c[0] + c[1] * y2) * pw - c[2] * (1.0 + c[9] * y2) - c[3] / y1 -
                            c[4] * y2 / y1 - (1.0 - c[9] * y2 / 3.0) * 1.5 * y2 * y2 -
                            (c[5] * s1 + c[6] * s2) * (1.0 + c[9] * y2) - y1 * (c[7] * c1 + c[8] * c2);
     const Real denominator = y1 - c[9] * y1 * y2 + c[4] * c[9];

@@ -158,3 +158,7 @@ void download_outcomes(odegpu_batch* b, Index start, Index count, odegpu_outcome
 void release_batch_stage(odegpu_batch* b);
 
 } // namespace odegpu::detail
+
+namespace odegpu::detail {
+void run_math_check(int fn, Index n, const double* x, const double* y, double* mine, double* ref);
+} // namespace odegpu::detail
