@@ -244,6 +244,14 @@ def _bind(lib):
             [P(PoolView), P(PoolOut), P(Model), P(SolverConfig), P(OdeControls), P(EventControls), Index, Index,
              Index, C.c_uint32, CHUNK_SINK, vp, P(C.c_int), C.c_int],
         ),
+        "odegpu_pipeline_create": (C.c_int, [P(Model), Index, C.c_int, P(vp)]),
+        "odegpu_pipeline_run": (
+            C.c_int,
+            [vp, P(PoolView), P(PoolOut), P(SolverConfig), P(OdeControls), P(EventControls), Index, Index,
+             C.c_uint32, CHUNK_SINK, vp],
+        ),
+        "odegpu_pipeline_destroy": (None, [vp]),
+        "odegpu_math_check": (C.c_int, [C.c_int, Index, vp, vp, vp, vp]),
         "odegpu_slice": (C.c_int, [Index, C.c_int, C.c_int, P(Index), P(Index)]),
         "odegpu_host_register": (C.c_int, [vp, C.c_size_t]),
         "odegpu_host_unregister": (C.c_int, [vp]),

@@ -398,28 +398,18 @@ def slice_range(total: int, parts: int, index: int) -> tuple[int, int]:
 RECORD_TD, RECORD_STATE, RECORD_ACC, RECORD_OUTCOMES = 1, 2, 8, 16
 
 
-def solve_pool(pool: ProblemPool, defn: SystemDef, cfg: SolverConfig | None, batch_capacity: int, iterations: int,
-               *, record_from: int | None = None, record_mask: int = 0, on_chunk=None, write_back: bool = True,
-               devices=(0,)):
-    """Chunked pool pipeline (odegpu_solve_pool[_multi]): the pool runs through
-    the device(s) in chunks of `batch_capacity`, `iterations` solves each,
-    with double-buffered copies. Returns (td, state, acc, outcomes) endpoint
-    arrays (pool layout) if `write_back`. `on_chunk(start, count, records)`
-    receives, per chunk, a dict of recorded per-iteration arrays."""
-    cfg = cfg or SolverConfig()
-    ode, ev = _controls(defn)
+def _pool_out(defn, n, arrays=None):
     d = defn.dims()
-    n = pool.size()
-    record_from = iterations if record_from is None else record_from
-    n_rec = iterations - record_from
-    out_arrays = None
-    out = None
-    if write_back:
-        out_arrays = (np.zeros(2 * n), np.zeros(d.system_dim * n), np.zeros(d.accessory_count * n),
-                      np.zeros(n, dtype=abi.OUTCOME_DTYPE))
-        out = abi.PoolOut(abi.dptr(out_arrays[0]), abi.dptr(out_arrays[1]),
-                          abi.dptr(out_arrays[2] if d.accessory_count else None), abi.vptr(out_arrays[3]))
-    err = []
+    if arrays is None:
+        arrays = (np.zeros(2 * n), np.zeros(d.system_dim * n), np.zeros(d.accessory_count * n),
+                  np.zeros(n, dtype=abi.OUTCOME_DTYPE))
+    out = abi.PoolOut(abi.dptr(arrays[0]), abi.dptr(arrays[1]), abi.dptr(arrays[2] if d.accessory_count else None),
+                      abi.vptr(arrays[3]))
+    return arrays, out
+
+
+def _chunk_sink(defn, record_mask, on_chunk, err):
+    d = defn.dims()
 
     def _sink(start, count, nrec, rec_p, _u):
         try:
@@ -440,7 +430,64 @@ def solve_pool(pool: ProblemPool, defn: SystemDef, cfg: SolverConfig | None, bat
             err.append(e)
             return 1
 
-    cb = abi.CHUNK_SINK(_sink) if on_chunk else abi.CHUNK_SINK()
+    return abi.CHUNK_SINK(_sink) if on_chunk else abi.CHUNK_SINK()
+
+
+class Pipeline:
+    """Persistent chunked pipeline (odegpu_pipeline_*): two device batches of
+    `batch_capacity` systems, two streams and pinned staging, reused by every
+    run() — chunk k+1's H2D and chunk k-1's D2H overlap chunk k's kernels."""
+
+    def __init__(self, defn: SystemDef, batch_capacity: int, device: int = 0):
+        self._lib = abi.load()
+        self.defn = defn
+        h = C.c_void_p()
+        check(self._lib.odegpu_pipeline_create(C.byref(defn.to_c()), batch_capacity, device, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.odegpu_pipeline_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def run(self, pool: ProblemPool, cfg: SolverConfig | None, iterations: int, *, record_from: int | None = None,
+            record_mask: int = 0, on_chunk=None, out_arrays=None):
+        cfg = cfg or SolverConfig()
+        ode, ev = _controls(self.defn)
+        record_from = iterations if record_from is None else record_from
+        arrays, out = _pool_out(self.defn, pool.size(), out_arrays)
+        err = []
+        cb = _chunk_sink(self.defn, record_mask, on_chunk, err)
+        rc = self._lib.odegpu_pipeline_run(self._h, C.byref(pool.view()), C.byref(out), C.byref(cfg.to_c()),
+                                           C.byref(ode), C.byref(ev), iterations, record_from,
+                                           record_mask if on_chunk else 0, cb, None)
+        if err:
+            raise err[0]
+        check(rc)
+        return arrays
+
+
+def solve_pool(pool: ProblemPool, defn: SystemDef, cfg: SolverConfig | None, batch_capacity: int, iterations: int,
+               *, record_from: int | None = None, record_mask: int = 0, on_chunk=None, write_back: bool = True,
+               devices=(0,)):
+    """Chunked pool pipeline (odegpu_solve_pool[_multi]): the pool runs through
+    the device(s) in chunks of `batch_capacity`, `iterations` solves each,
+    with double-buffered copies. Returns (td, state, acc, outcomes) endpoint
+    arrays (pool layout) if `write_back`. `on_chunk(start, count, records)`
+    receives, per chunk, a dict of recorded per-iteration arrays."""
+    cfg = cfg or SolverConfig()
+    ode, ev = _controls(defn)
+    n = pool.size()
+    record_from = iterations if record_from is None else record_from
+    out_arrays, out = _pool_out(defn, n) if write_back else (None, None)
+    err = []
+    cb = _chunk_sink(defn, record_mask, on_chunk, err)
     lib = abi.load()
     args = (C.byref(pool.view()), C.byref(out) if out is not None else None, C.byref(defn.to_c()),
             C.byref(cfg.to_c()), C.byref(ode), C.byref(ev), batch_capacity, iterations, record_from,

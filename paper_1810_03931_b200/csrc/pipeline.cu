@@ -89,128 +89,193 @@ void release_batch_stage(odegpu_batch* b) {
 
 namespace {
 
-/// Host staging of one pipeline slot (pinned).
+double* pinned(Index doubles) {
+    double* p = nullptr;
+    if (doubles > 0) CK(cudaMallocHost(&p, size_t(doubles) * 8));
+    return p;
+}
+
+/// One half of the double buffer: a device batch plus pinned staging.
 struct Slot {
     odegpu_batch* batch = nullptr;
     cudaEvent_t done = nullptr;
-    double* rec_td = nullptr;   // [n_rec][2][cap]
-    double* rec_y = nullptr;    // [n_rec][dim][cap]
-    double* rec_acc = nullptr;  // [n_rec][acc][cap]
-    std::vector<OutcomeStage> rec_out;
-    double* fin_td = nullptr;   // [2][cap]
+    double* fin_td = nullptr; // endpoints of the chunk, [comps][cap]
     double* fin_y = nullptr;
     double* fin_acc = nullptr;
     OutcomeStage fin_out;
+    double* rec_td = nullptr; // recorded iterations, [n_rec][comps][cap]
+    double* rec_y = nullptr;
+    double* rec_acc = nullptr;
+    std::vector<OutcomeStage> rec_out;
     Index start = 0, count = 0;
     bool busy = false;
 };
 
-struct PoolJob {
+struct Run {
     const odegpu_pool_view* pool;
     const odegpu_pool_out* out;
-    const odegpu_model* model;
     const odegpu_solver_config* cfg;
     const odegpu_ode_controls* ode;
     const odegpu_event_controls* ev;
-    Index capacity, iterations, record_from;
+    Index iterations, record_from;
     uint32_t mask;
     odegpu_chunk_sink sink;
     void* user;
     std::mutex* sink_mutex; // serialises sinks across device threads
 };
 
-/// Runs systems [begin, end) of the pool on `device`.
-void run_range(const PoolJob& j, Index begin, Index end, int device) {
+} // namespace
+} // namespace odegpu::detail
+
+/// The pipeline object: everything a chunked run needs, allocated once.
+struct odegpu_pipeline {
+    odegpu_model model{};
+    odegpu_system_dims sd{};
+    Index cap = 0;
+    int device = 0;
+    Index rec_capacity = 0; // recorded iterations the staging can hold
+    odegpu::detail::Slot slots[2];
+    std::vector<odegpu_outcome> packed;
+
+    ~odegpu_pipeline() {
+        for (auto& s : slots) {
+            if (s.batch) {
+                cudaStreamSynchronize(s.batch->stream);
+                odegpu_batch_destroy(s.batch);
+            }
+            if (s.done) cudaEventDestroy(s.done);
+            for (double* p : {s.fin_td, s.fin_y, s.fin_acc, s.rec_td, s.rec_y, s.rec_acc})
+                if (p) cudaFreeHost(p);
+            s.fin_out.release();
+            for (auto& o : s.rec_out) o.release();
+        }
+    }
+};
+
+namespace odegpu::detail {
+namespace {
+
+odegpu_pipeline* pipeline_create(const odegpu_model& model, Index capacity, int device) {
+    if (capacity < 1) throw_invalid("BatchDims: batch_capacity must be >= 1");
+    auto* p = new odegpu_pipeline;
+    try {
+        p->model = model;
+        p->sd = dims_of(model);
+        p->cap = capacity;
+        p->device = device;
+        DeviceGuard g(device);
+        const auto& sd = p->sd;
+        const odegpu_batch_dims bd{capacity, sd.system_dim, sd.param_count, sd.event_count, sd.accessory_count};
+        for (auto& s : p->slots) {
+            s.batch = batch_create(bd, device);
+            CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+            s.fin_td = pinned(2 * capacity);
+            s.fin_y = pinned(sd.system_dim * capacity);
+            s.fin_acc = pinned(sd.accessory_count * capacity);
+            s.fin_out.allocate(capacity);
+        }
+    } catch (...) {
+        delete p;
+        throw;
+    }
+    return p;
+}
+
+/// Grow the recorded-iteration staging to n_rec iterations.
+void reserve_records(odegpu_pipeline* p, Index n_rec, uint32_t mask) {
+    if (n_rec <= p->rec_capacity) return;
+    const auto& sd = p->sd;
+    const Index cap = p->cap;
+    for (auto& s : p->slots) {
+        for (double* q : {s.rec_td, s.rec_y, s.rec_acc})
+            if (q) cudaFreeHost(q);
+        s.rec_td = s.rec_y = s.rec_acc = nullptr;
+        for (auto& o : s.rec_out) o.release();
+        s.rec_out.clear();
+        if (mask & 1u) s.rec_td = pinned(n_rec * 2 * cap);
+        if (mask & 2u) s.rec_y = pinned(n_rec * sd.system_dim * cap);
+        if (mask & 8u) s.rec_acc = pinned(n_rec * sd.accessory_count * cap);
+        if (mask & 16u) {
+            s.rec_out.resize(size_t(n_rec));
+            for (auto& o : s.rec_out) o.allocate(cap);
+        }
+    }
+    p->rec_capacity = n_rec;
+    p->packed.resize(size_t(n_rec * cap));
+}
+
+/// Runs systems [begin, end) of the pool through the pipeline's device.
+void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
     const odegpu_pool_dims& pd = j.pool->dims;
-    const odegpu_system_dims sd = dims_of(*j.model);
+    const odegpu_system_dims& sd = p->sd;
     if (sd.system_dim != pd.system_dim || sd.param_count != pd.param_count ||
         sd.accessory_count != pd.accessory_count)
         throw_invalid("solve_pool: definition and pool dimensions disagree");
-    const Index total = end - begin;
-    if (total <= 0) return;
-    const Index cap = std::min(j.capacity, total);
+    if (end <= begin) return;
+    const Index cap = p->cap;
     const odegpu_batch_dims bd{cap, sd.system_dim, sd.param_count, sd.event_count, sd.accessory_count};
-    const dev::Controls c = prepare_solve(bd, j.model, j.cfg, j.ode, j.ev);
-    const Index n_rec = j.iterations - j.record_from;
+    const dev::Controls c = prepare_solve(bd, &p->model, j.cfg, j.ode, j.ev);
+    const Index n_rec = j.sink ? j.iterations - j.record_from : 0;
+    const uint32_t mask = j.sink ? j.mask : 0u;
     const Index N = pd.problem_size;
-    const bool r_td = j.mask & 1u, r_y = j.mask & 2u, r_acc = (j.mask & 8u) && sd.accessory_count,
-               r_out = j.mask & 16u;
+    const bool r_td = mask & 1u, r_y = mask & 2u, r_acc = (mask & 8u) && sd.accessory_count, r_out = mask & 16u;
+    DeviceGuard g(p->device);
+    if (n_rec > 0) {
+        // (re)allocate when the mask needs arrays the staging lacks
+        const Slot& s0 = p->slots[0];
+        const bool lacking = (r_td && !s0.rec_td) || (r_y && !s0.rec_y) || (r_acc && !s0.rec_acc) ||
+                             (r_out && s0.rec_out.empty());
+        if (lacking) p->rec_capacity = 0;
+        reserve_records(p, n_rec, mask);
+    }
 
-    DeviceGuard g(device);
-    Slot slots[2];
-    auto cleanup = [&] {
-        for (auto& s : slots) {
-            if (s.batch) odegpu_batch_destroy(s.batch);
-            if (s.done) cudaEventDestroy(s.done);
-            for (double* p : {s.rec_td, s.rec_y, s.rec_acc, s.fin_td, s.fin_y, s.fin_acc})
-                if (p) cudaFreeHost(p);
-            for (auto& o : s.rec_out) o.release();
-            s.fin_out.release();
+    // Consume a finished slot: validation flag, write-back, sink.
+    auto drain = [&](Slot& s) {
+        if (!s.busy) return;
+        CK(cudaEventSynchronize(s.done));
+        s.busy = false;
+        if (*s.batch->host_flag != ~0ull)
+            throw_invalid("solve: system " + std::to_string(static_cast<long long>(*s.batch->host_flag)) +
+                          " has t1 < t0");
+        const Index n = s.count, off = s.start;
+        auto put = [&](double* dst, const double* src, Index comps) {
+            if (!dst) return;
+            for (Index cc = 0; cc < comps; ++cc) std::memcpy(dst + off + cc * N, src + cc * cap, size_t(n) * 8);
+        };
+        if (j.out) {
+            put(j.out->time_domain, s.fin_td, 2);
+            put(j.out->state, s.fin_y, sd.system_dim);
+            if (sd.accessory_count) put(j.out->accessories, s.fin_acc, sd.accessory_count);
+            if (j.out->outcomes) s.fin_out.pack(j.out->outcomes + off, n);
+        }
+        if (j.sink && n_rec > 0) {
+            if (r_out)
+                for (Index r = 0; r < n_rec; ++r) s.rec_out[size_t(r)].pack(p->packed.data() + r * n, n);
+            // compact the recorded arrays from stride cap to stride n
+            auto compact = [&](double* q, Index comps) {
+                if (!q || n == cap) return;
+                for (Index r = 0; r < n_rec; ++r)
+                    for (Index cc = 0; cc < comps; ++cc)
+                        std::memmove(q + (r * comps + cc) * n, q + (r * comps + cc) * cap, size_t(n) * 8);
+            };
+            if (r_td) compact(s.rec_td, 2);
+            if (r_y) compact(s.rec_y, sd.system_dim);
+            if (r_acc) compact(s.rec_acc, sd.accessory_count);
+            const odegpu_chunk_record rec{r_td ? s.rec_td : nullptr, r_y ? s.rec_y : nullptr,
+                                          r_acc ? s.rec_acc : nullptr, r_out ? p->packed.data() : nullptr};
+            int rc;
+            {
+                std::lock_guard<std::mutex> lock(*j.sink_mutex);
+                rc = j.sink(off, n, n_rec, &rec, j.user);
+            }
+            if (rc != 0) throw Error(rc, "solve_pool: chunk sink returned " + std::to_string(rc));
         }
     };
+
+    int k = 0;
     try {
-        for (auto& s : slots) {
-            s.batch = batch_create(bd, device);
-            CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
-            auto pin = [&](double** p, Index doubles) {
-                if (doubles > 0) CK(cudaMallocHost(p, size_t(doubles) * 8));
-            };
-            if (r_td) pin(&s.rec_td, n_rec * 2 * cap);
-            if (r_y) pin(&s.rec_y, n_rec * sd.system_dim * cap);
-            if (r_acc) pin(&s.rec_acc, n_rec * sd.accessory_count * cap);
-            if (r_out) {
-                s.rec_out.resize(size_t(n_rec));
-                for (auto& o : s.rec_out) o.allocate(cap);
-            }
-            if (j.out && j.out->time_domain) pin(&s.fin_td, 2 * cap);
-            if (j.out && j.out->state) pin(&s.fin_y, sd.system_dim * cap);
-            if (j.out && j.out->accessories && sd.accessory_count) pin(&s.fin_acc, sd.accessory_count * cap);
-            if (j.out && j.out->outcomes) s.fin_out.allocate(cap);
-        }
-
-        std::vector<odegpu_outcome> packed(size_t(cap) * size_t(std::max<Index>(n_rec, 1)));
-        // Consume a finished slot: validation flag, write-back, sink.
-        auto drain = [&](Slot& s) {
-            if (!s.busy) return;
-            CK(cudaEventSynchronize(s.done));
-            s.busy = false;
-            if (*s.batch->host_flag != ~0ull)
-                throw_invalid("solve: system " + std::to_string(static_cast<long long>(*s.batch->host_flag)) +
-                              " has t1 < t0");
-            const Index n = s.count, off = s.start;
-            auto put = [&](double* dst, const double* src, Index comps) {
-                for (Index cc = 0; cc < comps; ++cc) std::memcpy(dst + off + cc * N, src + cc * cap, size_t(n) * 8);
-            };
-            if (s.fin_td) put(j.out->time_domain, s.fin_td, 2);
-            if (s.fin_y) put(j.out->state, s.fin_y, sd.system_dim);
-            if (s.fin_acc) put(j.out->accessories, s.fin_acc, sd.accessory_count);
-            if (s.fin_out.block) s.fin_out.pack(j.out->outcomes + off, n);
-            if (j.sink && n_rec > 0) {
-                if (r_out)
-                    for (Index r = 0; r < n_rec; ++r) s.rec_out[size_t(r)].pack(packed.data() + r * n, n);
-                // compact the recorded arrays from stride cap to stride n
-                auto compact = [&](double* p, Index comps) {
-                    if (!p || n == cap) return;
-                    for (Index r = 0; r < n_rec; ++r)
-                        for (Index cc = 0; cc < comps; ++cc)
-                            std::memmove(p + (r * comps + cc) * n, p + (r * comps + cc) * cap, size_t(n) * 8);
-                };
-                compact(s.rec_td, 2);
-                compact(s.rec_y, sd.system_dim);
-                compact(s.rec_acc, sd.accessory_count);
-                const odegpu_chunk_record rec{s.rec_td, s.rec_y, s.rec_acc, r_out ? packed.data() : nullptr};
-                int rc;
-                {
-                    std::lock_guard<std::mutex> lock(*j.sink_mutex);
-                    rc = j.sink(off, n, n_rec, &rec, j.user);
-                }
-                if (rc != 0) throw Error(rc, "solve_pool: chunk sink returned " + std::to_string(rc));
-            }
-        };
-
-        int k = 0;
         for (Index start = begin; start < end; start += cap, ++k) {
-            Slot& s = slots[k & 1];
+            Slot& s = p->slots[k & 1];
             drain(s); // the slot's previous chunk must be consumed before reuse
             odegpu_batch* b = s.batch;
             const Index n = std::min(cap, end - start);
@@ -228,8 +293,8 @@ void run_range(const PoolJob& j, Index begin, Index end, int device) {
             launch_reset_outcomes(b, 0, n);
             for (Index it = 0; it < j.iterations; ++it) {
                 enqueue_time_check(b);
-                launch_model(b, *j.model, j.cfg->algorithm, c);
-                if (it >= j.record_from) {
+                launch_model(b, p->model, j.cfg->algorithm, c);
+                if (n_rec > 0 && it >= j.record_from) {
                     const Index r = it - j.record_from;
                     if (r_td) copy_d2h_strided(s.rec_td + r * 2 * cap, cap, 0, b->a.td, cap, 0, n, 2, b->stream);
                     if (r_y)
@@ -241,37 +306,38 @@ void run_range(const PoolJob& j, Index begin, Index end, int device) {
                     if (r_out) s.rec_out[size_t(r)].fetch(b, 0, n, b->stream);
                 }
             }
-            if (s.fin_td) copy_d2h_strided(s.fin_td, cap, 0, b->a.td, cap, 0, n, 2, b->stream);
-            if (s.fin_y) copy_d2h_strided(s.fin_y, cap, 0, b->a.state, cap, 0, n, sd.system_dim, b->stream);
-            if (s.fin_acc)
-                copy_d2h_strided(s.fin_acc, cap, 0, b->a.acc, cap, 0, n, sd.accessory_count, b->stream);
-            if (s.fin_out.block) s.fin_out.fetch(b, 0, n, b->stream);
+            if (j.out) {
+                if (j.out->time_domain) copy_d2h_strided(s.fin_td, cap, 0, b->a.td, cap, 0, n, 2, b->stream);
+                if (j.out->state) copy_d2h_strided(s.fin_y, cap, 0, b->a.state, cap, 0, n, sd.system_dim, b->stream);
+                if (j.out->accessories && sd.accessory_count)
+                    copy_d2h_strided(s.fin_acc, cap, 0, b->a.acc, cap, 0, n, sd.accessory_count, b->stream);
+                if (j.out->outcomes) s.fin_out.fetch(b, 0, n, b->stream);
+            }
             CK(cudaMemcpyAsync(b->host_flag, b->first_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                b->stream));
             CK(cudaEventRecord(s.done, b->stream));
             s.busy = true;
-            // chunk k-1 (other slot) is drained at the top of iteration k+1, so
-            // its D2H and the host work overlap chunk k's kernels
+            // chunk k-1 (the other slot) is drained at the top of the next
+            // iteration, so its D2H and host work overlap chunk k's kernels
         }
-        drain(slots[k & 1]); // oldest first
-        drain(slots[(k + 1) & 1]);
+        drain(p->slots[k & 1]); // oldest first
+        drain(p->slots[(k + 1) & 1]);
     } catch (...) {
-        for (auto& s : slots)
+        for (auto& s : p->slots) {
             if (s.batch) cudaStreamSynchronize(s.batch->stream);
-        cleanup();
+            s.busy = false;
+        }
         throw;
     }
-    cleanup();
 }
 
-void validate_job(const PoolJob& j) {
-    if (!j.pool || !j.model || !j.cfg || !j.ode) throw_invalid("solve_pool: null argument");
-    if (j.capacity < 1) throw_invalid("BatchDims: batch_capacity must be >= 1");
-    if (j.iterations < 1) throw_invalid("solve_iteratively: iterations must be >= 1");
-    if (j.record_from < 0 || j.record_from > j.iterations)
-        throw_invalid("solve_pool: record_from outside [0, iterations]");
-    if (j.pool->dims.problem_size < 1) throw_invalid("PoolDims: problem_size must be >= 1");
-    if (!j.pool->time_domain || !j.pool->state) throw_invalid("solve_pool: pool arrays missing");
+void validate_run(const odegpu_pool_view* pool, const odegpu_solver_config* cfg, const odegpu_ode_controls* ode,
+                  Index iterations, Index record_from) {
+    if (!pool || !cfg || !ode) throw_invalid("solve_pool: null argument");
+    if (iterations < 1) throw_invalid("solve_iteratively: iterations must be >= 1");
+    if (record_from < 0 || record_from > iterations) throw_invalid("solve_pool: record_from outside [0, iterations]");
+    if (pool->dims.problem_size < 1) throw_invalid("PoolDims: problem_size must be >= 1");
+    if (!pool->time_domain || !pool->state) throw_invalid("solve_pool: pool arrays missing");
 }
 
 } // namespace
@@ -300,17 +366,56 @@ int odegpu_slice(odegpu_index total, int parts, int index, odegpu_index* begin, 
     });
 }
 
+int odegpu_pipeline_create(const odegpu_model* model, odegpu_index batch_capacity, int device,
+                           odegpu_pipeline** out) {
+    return guarded([&] {
+        if (!model || !out) throw_invalid("null argument");
+        *out = nullptr;
+        *out = pipeline_create(*model, batch_capacity, device);
+    });
+}
+
+void odegpu_pipeline_destroy(odegpu_pipeline* p) {
+    if (!p) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(p->device);
+    delete p;
+    if (prev >= 0) cudaSetDevice(prev);
+}
+
+int odegpu_pipeline_run(odegpu_pipeline* p, const odegpu_pool_view* pool, const odegpu_pool_out* out,
+                        const odegpu_solver_config* cfg, const odegpu_ode_controls* ode,
+                        const odegpu_event_controls* ev, odegpu_index iterations, odegpu_index record_from,
+                        uint32_t record_mask, odegpu_chunk_sink on_chunk, void* user) {
+    return guarded([&] {
+        if (!p) throw_invalid("null pipeline");
+        validate_run(pool, cfg, ode, iterations, record_from);
+        std::mutex mu;
+        const Run j{pool, out, cfg, ode, ev, iterations, record_from, record_mask, on_chunk, user, &mu};
+        run_range(p, j, 0, pool->dims.problem_size);
+    });
+}
+
 int odegpu_solve_pool(const odegpu_pool_view* pool, const odegpu_pool_out* out, const odegpu_model* model,
                       const odegpu_solver_config* cfg, const odegpu_ode_controls* ode,
                       const odegpu_event_controls* ev, odegpu_index batch_capacity, odegpu_index iterations,
                       odegpu_index record_from, uint32_t record_mask, odegpu_chunk_sink on_chunk, void* user,
                       int device) {
     return guarded([&] {
+        if (!model) throw_invalid("solve_pool: null argument");
+        validate_run(pool, cfg, ode, iterations, record_from);
+        const Index cap = batch_capacity < 1 ? batch_capacity : std::min<Index>(batch_capacity, pool->dims.problem_size);
+        odegpu_pipeline* p = pipeline_create(*model, cap, device);
         std::mutex mu;
-        const PoolJob j{pool, out, model, cfg, ode, ev, batch_capacity, iterations, record_from, record_mask,
-                        on_chunk, user, &mu};
-        validate_job(j);
-        run_range(j, 0, pool->dims.problem_size, device);
+        const Run j{pool, out, cfg, ode, ev, iterations, record_from, record_mask, on_chunk, user, &mu};
+        try {
+            run_range(p, j, 0, pool->dims.problem_size);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        delete p;
     });
 }
 
@@ -321,24 +426,31 @@ int odegpu_solve_pool_multi(const odegpu_pool_view* pool, const odegpu_pool_out*
                             odegpu_chunk_sink on_chunk, void* user, const int* devices, int n_devices) {
     return guarded([&] {
         if (!devices || n_devices < 1) throw_invalid("solve_pool_multi: no devices");
+        if (!model) throw_invalid("solve_pool: null argument");
+        validate_run(pool, cfg, ode, iterations, record_from);
+        if (batch_capacity < 1) throw_invalid("BatchDims: batch_capacity must be >= 1");
         std::mutex mu;
-        const PoolJob j{pool, out, model, cfg, ode, ev, batch_capacity, iterations, record_from, record_mask,
-                        on_chunk, user, &mu};
-        validate_job(j);
+        const Run j{pool, out, cfg, ode, ev, iterations, record_from, record_mask, on_chunk, user, &mu};
         std::exception_ptr* failures = new std::exception_ptr[size_t(n_devices)];
         std::vector<std::thread> threads;
         for (int d = 0; d < n_devices; ++d) {
             Index b0 = 0, b1 = 0;
             odegpu_slice(pool->dims.problem_size, n_devices, d, &b0, &b1);
-            const PoolJob* jp = &j;
+            const Run* jp = &j;
             std::exception_ptr* slot = failures + d;
             const int dev_id = devices[d];
-            threads.emplace_back([jp, slot, dev_id, b0, b1] {
+            const odegpu_model m = *model;
+            threads.emplace_back([jp, slot, dev_id, b0, b1, m, batch_capacity] {
+                odegpu_pipeline* p = nullptr;
                 try {
-                    run_range(*jp, b0, b1, dev_id);
+                    if (b1 > b0) {
+                        p = pipeline_create(m, std::min<Index>(batch_capacity, b1 - b0), dev_id);
+                        run_range(p, *jp, b0, b1);
+                    }
                 } catch (...) {
                     *slot = std::current_exception();
                 }
+                delete p;
             });
         }
         for (auto& t : threads) t.join();

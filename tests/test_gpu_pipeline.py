@@ -62,6 +62,25 @@ def test_pipeline_equals_resident_batch(cfg, count, cap, its, devices):
             assert np.array_equal(outcome_bytes(got_o), outcome_bytes(so[s:s + n]))
 
 
+def test_persistent_pipeline_reuse():
+    """odegpu_pipeline_* keeps its batches/staging across runs: two different
+    pools, then the first again, reproduce the one-shot solve_pool bitwise."""
+    a = workloads.cfg4().strided(2000)
+    b = workloads.cfg4().subset(slice(5000, 6500))
+    pools = [pkg.ProblemPool.from_arrays(*w.arrays()) for w in (a, b)]
+    cfg = pkg.SolverConfig(a.algorithm, a.dt)
+    want = [pkg.solve_pool(p, a.model, cfg, 600, 2) for p in pools]
+    pipe = pkg.api.Pipeline(a.model, 600)
+    recs = []
+    for i in (0, 1, 0):
+        got = pipe.run(pools[i], cfg, 2, record_from=1, record_mask=pkg.api.RECORD_STATE,
+                       on_chunk=lambda s, n, r: recs.append((s, n)))
+        for g, w in zip(got, want[i]):
+            assert np.array_equal(np.ascontiguousarray(g).view(np.uint8), np.ascontiguousarray(w).view(np.uint8))
+    assert sum(n for _, n in recs) == 2000 + 1500 + 2000
+    pipe.close()
+
+
 def test_pipeline_reports_bad_time_domain():
     wl = workloads.cfg2().strided(600)
     td, y, p, acc = wl.arrays()
