@@ -320,7 +320,8 @@ def main():
     h2d = (h_td.nbytes + h_y.nbytes + h_p.nbytes + h_a.nbytes)
     d2h = o_y.nbytes + o_td.nbytes + o_a.nbytes + n * abi.OUTCOME_DTYPE.itemsize
     e2e_steps, e2e_s = 0, 0.0
-    outc = np.zeros(n, dtype=abi.OUTCOME_DTYPE)
+    outc = torch.zeros(n * abi.OUTCOME_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True).numpy().view(
+        abi.OUTCOME_DTYPE)
     if world > 1:
         torch.distributed.barrier()
     # the chunked pool pipeline: 4 chunks, H2D of chunk k+1 and D2H of chunk

@@ -63,7 +63,7 @@ struct BatchArrays {
 };
 
 // --- Cash-Karp tableau (steppers.hpp:16-39): exact rationals rendered once.
-namespace ck {
+namespace ckv {
 constexpr Real c2 = 1.0 / 5.0, c3 = 3.0 / 10.0, c4 = 3.0 / 5.0, c5 = 1.0, c6 = 7.0 / 8.0;
 constexpr Real a21 = 1.0 / 5.0;
 constexpr Real a31 = 3.0 / 40.0, a32 = 9.0 / 40.0;
@@ -75,6 +75,21 @@ constexpr Real b1 = 37.0 / 378.0, b3 = 250.0 / 621.0, b4 = 125.0 / 594.0, b6 = 5
 constexpr Real e1 = 2825.0 / 27648.0, e3 = 18575.0 / 48384.0, e4 = 13525.0 / 55296.0, e5 = 277.0 / 14336.0,
                e6 = 1.0 / 4.0;
 constexpr Real d1 = b1 - e1, d3 = b3 - e3, d4 = b4 - e4, d5 = -e5, d6 = b6 - e6;
+} // namespace ckv
+
+/// The same values as the kernels read them: coefficients with long
+/// mantissas live in the constant bank, so ptxas folds them into c[][]
+/// operands of the DFMAs instead of two UMOVs per use; short ones (1, 7/8,
+/// 5/2) stay encodable immediates.
+namespace ck {
+static __constant__ Real c2 = ckv::c2, c3 = ckv::c3, c4 = ckv::c4;
+constexpr Real c5 = ckv::c5, c6 = ckv::c6;
+static __constant__ Real a21 = ckv::a21, a31 = ckv::a31, a32 = ckv::a32, a41 = ckv::a41, a42 = ckv::a42,
+                         a43 = ckv::a43, a51 = ckv::a51, a53 = ckv::a53, a54 = ckv::a54, a61 = ckv::a61,
+                         a62 = ckv::a62, a63 = ckv::a63, a64 = ckv::a64, a65 = ckv::a65;
+constexpr Real a52 = ckv::a52;
+static __constant__ Real b1 = ckv::b1, b3 = ckv::b3, b4 = ckv::b4, b6 = ckv::b6;
+static __constant__ Real d1 = ckv::d1, d3 = ckv::d3, d4 = ckv::d4, d5 = ckv::d5, d6 = ckv::d6;
 } // namespace ck
 
 // std::max / std::min / std::clamp semantics, including NaN behaviour.

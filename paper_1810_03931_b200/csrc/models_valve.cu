@@ -6,11 +6,12 @@
 namespace odegpu::detail {
 
 // Valve: small RHS, straight-line stages, cold state in shared memory,
-// 7 blocks/SM (72 registers; profiles/r01_variants.md: 3.49 ms vs 4.72 ms
-// all-register).
+// 6 blocks/SM (80 registers, spill-free; profiles/r01_variants.md: 3.60 ms
+// vs 4.72 ms all-register; 7 blocks spills 8 B since the constant-bank
+// tableau).
 template <>
 struct LaunchPolicy<models::ValveHooks> {
-    static constexpr int kMinBlocks = 7;
+    static constexpr int kMinBlocks = 6;
 };
 
 bool family_dims_valve(const odegpu_model& m, odegpu_system_dims* d) {

@@ -89,6 +89,33 @@ void release_batch_stage(odegpu_batch* b) {
 
 namespace {
 
+// AoS odensemble::SystemOutcome records (56 B) from the SoA outcome fields,
+// so one D2H lands them in the caller's array without host-side packing.
+__global__ void pack_outcomes_kernel(dev::BatchArrays b, Index count, odegpu_outcome* dst) {
+    for (Index i = blockIdx.x * static_cast<Index>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<Index>(gridDim.x) * blockDim.x) {
+        odegpu_outcome o{};
+        o.final_t = b.final_t[i];
+        o.reason = b.reason[i];
+        o.accepted_steps = b.accepted[i];
+        o.rejected_steps = b.rejected[i];
+        o.event_detections = b.detections[i];
+        o.secant_failures = b.secant_failures[i];
+        o.smallest_step = b.smallest_step[i];
+        dst[i] = o;
+    }
+}
+
+bool is_pinned(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 double* pinned(Index doubles) {
     double* p = nullptr;
     if (doubles > 0) CK(cudaMallocHost(&p, size_t(doubles) * 8));
@@ -102,7 +129,8 @@ struct Slot {
     double* fin_td = nullptr; // endpoints of the chunk, [comps][cap]
     double* fin_y = nullptr;
     double* fin_acc = nullptr;
-    OutcomeStage fin_out;
+    odegpu_outcome* d_packed = nullptr;   // device AoS outcome records [cap]
+    odegpu_outcome* fin_out = nullptr;    // pinned AoS staging [cap]
     double* rec_td = nullptr; // recorded iterations, [n_rec][comps][cap]
     double* rec_y = nullptr;
     double* rec_acc = nullptr;
@@ -146,7 +174,8 @@ struct odegpu_pipeline {
             if (s.done) cudaEventDestroy(s.done);
             for (double* p : {s.fin_td, s.fin_y, s.fin_acc, s.rec_td, s.rec_y, s.rec_acc})
                 if (p) cudaFreeHost(p);
-            s.fin_out.release();
+            if (s.fin_out) cudaFreeHost(s.fin_out);
+            if (s.d_packed) cudaFree(s.d_packed);
             for (auto& o : s.rec_out) o.release();
         }
     }
@@ -172,7 +201,8 @@ odegpu_pipeline* pipeline_create(const odegpu_model& model, Index capacity, int 
             s.fin_td = pinned(2 * capacity);
             s.fin_y = pinned(sd.system_dim * capacity);
             s.fin_acc = pinned(sd.accessory_count * capacity);
-            s.fin_out.allocate(capacity);
+            CK(cudaMallocHost(&s.fin_out, size_t(capacity) * sizeof(odegpu_outcome)));
+            CK(cudaMalloc(&s.d_packed, size_t(capacity) * sizeof(odegpu_outcome)));
         }
     } catch (...) {
         delete p;
@@ -229,7 +259,14 @@ void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
         reserve_records(p, n_rec, mask);
     }
 
-    // Consume a finished slot: validation flag, write-back, sink.
+    // Endpoint write-back: straight into the caller's arrays when they are
+    // page-locked (async D2H, no host copy), else via pinned staging.
+    const odegpu_pool_out none{};
+    const odegpu_pool_out& o = j.out ? *j.out : none;
+    const bool d_td = is_pinned(o.time_domain), d_y = is_pinned(o.state),
+               d_acc = sd.accessory_count && is_pinned(o.accessories), d_out = is_pinned(o.outcomes);
+
+    // Consume a finished slot: validation flag, staged write-back, sink.
     auto drain = [&](Slot& s) {
         if (!s.busy) return;
         CK(cudaEventSynchronize(s.done));
@@ -239,15 +276,12 @@ void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
                           " has t1 < t0");
         const Index n = s.count, off = s.start;
         auto put = [&](double* dst, const double* src, Index comps) {
-            if (!dst) return;
             for (Index cc = 0; cc < comps; ++cc) std::memcpy(dst + off + cc * N, src + cc * cap, size_t(n) * 8);
         };
-        if (j.out) {
-            put(j.out->time_domain, s.fin_td, 2);
-            put(j.out->state, s.fin_y, sd.system_dim);
-            if (sd.accessory_count) put(j.out->accessories, s.fin_acc, sd.accessory_count);
-            if (j.out->outcomes) s.fin_out.pack(j.out->outcomes + off, n);
-        }
+        if (o.time_domain && !d_td) put(o.time_domain, s.fin_td, 2);
+        if (o.state && !d_y) put(o.state, s.fin_y, sd.system_dim);
+        if (o.accessories && sd.accessory_count && !d_acc) put(o.accessories, s.fin_acc, sd.accessory_count);
+        if (o.outcomes && !d_out) std::memcpy(o.outcomes + off, s.fin_out, size_t(n) * sizeof(odegpu_outcome));
         if (j.sink && n_rec > 0) {
             if (r_out)
                 for (Index r = 0; r < n_rec; ++r) s.rec_out[size_t(r)].pack(p->packed.data() + r * n, n);
@@ -306,12 +340,26 @@ void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
                     if (r_out) s.rec_out[size_t(r)].fetch(b, 0, n, b->stream);
                 }
             }
-            if (j.out) {
-                if (j.out->time_domain) copy_d2h_strided(s.fin_td, cap, 0, b->a.td, cap, 0, n, 2, b->stream);
-                if (j.out->state) copy_d2h_strided(s.fin_y, cap, 0, b->a.state, cap, 0, n, sd.system_dim, b->stream);
-                if (j.out->accessories && sd.accessory_count)
+            if (o.time_domain) {
+                if (d_td) copy_d2h_strided(o.time_domain, N, start, b->a.td, cap, 0, n, 2, b->stream);
+                else copy_d2h_strided(s.fin_td, cap, 0, b->a.td, cap, 0, n, 2, b->stream);
+            }
+            if (o.state) {
+                if (d_y) copy_d2h_strided(o.state, N, start, b->a.state, cap, 0, n, sd.system_dim, b->stream);
+                else copy_d2h_strided(s.fin_y, cap, 0, b->a.state, cap, 0, n, sd.system_dim, b->stream);
+            }
+            if (o.accessories && sd.accessory_count) {
+                if (d_acc)
+                    copy_d2h_strided(o.accessories, N, start, b->a.acc, cap, 0, n, sd.accessory_count, b->stream);
+                else
                     copy_d2h_strided(s.fin_acc, cap, 0, b->a.acc, cap, 0, n, sd.accessory_count, b->stream);
-                if (j.out->outcomes) s.fin_out.fetch(b, 0, n, b->stream);
+            }
+            if (o.outcomes) {
+                pack_outcomes_kernel<<<grid_for(b, n, 256), 256, 0, b->stream>>>(b->a, n, s.d_packed);
+                CK(cudaGetLastError());
+                ++b->launches;
+                CK(cudaMemcpyAsync(d_out ? o.outcomes + start : s.fin_out, s.d_packed,
+                                   size_t(n) * sizeof(odegpu_outcome), cudaMemcpyDeviceToHost, b->stream));
             }
             CK(cudaMemcpyAsync(b->host_flag, b->first_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                b->stream));
