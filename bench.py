@@ -14,9 +14,10 @@ the local-maximum EventFunction and event-time accessories on a 1024 x 1024
   of device time with the batch resident in HBM; timed with CUDA events on the
   batch's stream around each solve, L2 flushed (256 MiB write) between steps
   outside the events.
-* e2e: the same metric through the C ABI with host (pinned) buffers:
-  linear_set H2D of the pool, solve, D2H of state/accessories/time domains
-  and outcomes, per step, wall-clock.
+* e2e: the same metric through the C ABI with host (pinned) buffers: the
+  chunked pool pipeline (odegpu_pipeline_run, 4 chunks) — H2D of the pool,
+  solve, D2H of time domains / state / accessories / outcome records into
+  host arrays, per step, wall-clock.
 * roofline: FP64-pipe lane instructions per trial step (SURVEY.md §8d
   algorithmic count) / solve-kernel time vs the DFMA microbenchmark peak.
 * cpu_baseline: the reference solver (oracle/_ref, compiled from the
@@ -222,7 +223,11 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        import torch
+
+        # one rank per GPU: NCCL; ranks sharing a GPU (single-GPU test runs): gloo
+        shared = torch.cuda.device_count() < world
+        dist.init_process_group("nccl" if args.impl == "ours" and not shared else "gloo")
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         if world > 1:
@@ -233,8 +238,9 @@ def main():
 
     import torch
 
-    torch.cuda.set_device(local)
-    device = local
+    device = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(device)
+    red_dev = f"cuda:{device}" if world > 1 and torch.distributed.get_backend() == "nccl" else "cpu"
     log(f"torch ready, rank {rank}/{world} on cuda:{local}")
     wl = make_workload(args.config, rank, world)
     n = wl.n
@@ -293,10 +299,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([elapsed, kernel_s], dtype=torch.float64, device=f"cuda:{device}")
+        t = torch.tensor([elapsed, kernel_s], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed, kernel_s = float(t[0]), float(t[1])
-        c = torch.tensor([steps_total, sys_total], dtype=torch.float64, device=f"cuda:{device}")
+        c = torch.tensor([steps_total, sys_total], dtype=torch.float64, device=red_dev)
         dist.all_reduce(c, op=dist.ReduceOp.SUM)
         steps_total, sys_total = int(c[0]), int(c[1])
 
@@ -340,7 +346,7 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([e2e_s, e2e_steps], dtype=torch.float64, device=f"cuda:{device}")
+        t = torch.tensor([e2e_s, e2e_steps], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t[0])
         e2e_steps = e2e_steps * world  # weak scaling: every rank did its share
