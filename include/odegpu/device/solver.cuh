@@ -22,6 +22,7 @@
 #include <cstdint>
 #include <span>
 
+#include "odegpu.h"
 #include "odegpu/device/dmath.cuh"
 #include "odegpu/hooks.hpp"
 
@@ -779,9 +780,37 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
 #undef ODEGPU_C
 }
 
+/// The solve kernel. `skip` is the result of the t1 < t0 check queued
+/// before it: when a system failed it, nothing is integrated (the reference
+/// throws before solving, solve.hpp:159-161).
 template <class H, Algorithm ALG, int BLOCK, int MIN_BLOCKS>
-__global__ void __launch_bounds__(BLOCK, MIN_BLOCKS) solve_kernel(H model, BatchArrays b, Controls c) {
+__global__ void __launch_bounds__(BLOCK, MIN_BLOCKS)
+    guarded_solve_kernel(H model, BatchArrays b, Controls c, const unsigned long long* skip) {
+    if (*skip != ~0ull) return;
     solve_lanes<H, ALG, BLOCK>(model, b, c);
+}
+
+/// Kernel controls from the C-ABI structs (materialised once per solve,
+/// solve.hpp:153-155); the caller has validated them.
+inline Controls controls_from(const odegpu_system_dims& sys, const odegpu_solver_config& cfg,
+                              const odegpu_ode_controls& ode, const odegpu_event_controls* ev) {
+    Controls c{};
+    for (Index i = 0; i < sys.system_dim; ++i) {
+        c.rel_tol[i] = ode.rel_tol[i];
+        c.abs_tol[i] = ode.abs_tol[i];
+    }
+    c.max_step = ode.max_step;
+    c.min_step = ode.min_step;
+    c.step_grow_limit = ode.step_grow_limit;
+    c.step_shrink_limit = ode.step_shrink_limit;
+    c.initial_time_step = cfg.initial_time_step;
+    c.max_steps_in_zone = ev ? ev->max_steps_in_zone : 50;
+    for (Index i = 0; i < sys.event_count; ++i) {
+        c.direction[i] = ev->direction[i];
+        c.tolerance[i] = ev->tolerance[i];
+        c.stop_condition[i] = ev->stop_condition[i];
+    }
+    return c;
 }
 
 } // namespace odegpu::device

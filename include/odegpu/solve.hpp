@@ -11,6 +11,7 @@
 #define ODEGPU_SOLVE_HPP
 
 #include <exception>
+#include <type_traits>
 #include <stdexcept>
 #include <utility>
 #include <vector>
@@ -54,32 +55,39 @@ constexpr unsigned kSolveWrites = 0x1Bu; // time domain, state, accessories, out
 
 } // namespace detail
 
-/// Integrates every system of the batch on the GPU (solve.hpp:60-128).
+/// User-defined models are solved by a kernel instantiated in the caller's
+/// nvcc translation unit: include "odegpu/device/custom.cuh" there.
 template <SystemModel D>
-void solve(SolverBatch& batch, const D& def, const SolverConfig& cfg = {}) {
-    detail::CControls c(def, cfg);
+void solve_custom(SolverBatch& batch, const D& def, const SolverConfig& cfg);
+
+namespace detail {
+
+template <BuiltinModel D>
+void solve_builtin(SolverBatch& batch, const D& def, const SolverConfig& cfg) {
+    CControls c(def, cfg);
     const odegpu_model m = def.descriptor();
     batch.push();
     const int rc = odegpu_solve(batch.handle(), &m, &c.c_cfg, &c.c_ode, &c.c_ev);
-    batch.invalidate_host(detail::kSolveWrites);
-    detail::check(rc);
+    batch.invalidate_host(kSolveWrites);
+    check(rc);
 }
 
-/// solve.hpp:133-142: `iterations` solves, sink(i, const batch&) after each.
-template <SystemModel D, typename Sink>
-void solve_iteratively(SolverBatch& batch, const D& def, const SolverConfig& cfg, Index iterations, Sink&& sink) {
-    if (iterations < 1) throw std::invalid_argument("solve_iteratively: iterations must be >= 1");
-    detail::CControls c(def, cfg);
+/// odegpu_solve_iteratively with a C trampoline around the C++ sink (NULL
+/// sink when `sink` is null: iterations back to back on the device).
+template <BuiltinModel D, typename Sink>
+void solve_iteratively_builtin(SolverBatch& batch, const D& def, const SolverConfig& cfg, Index iterations,
+                               Sink* sink) {
+    CControls c(def, cfg);
     const odegpu_model m = def.descriptor();
     batch.push();
     struct Ctx {
         SolverBatch* batch;
         Sink* sink;
         std::exception_ptr error;
-    } ctx{&batch, &sink, nullptr};
+    } ctx{&batch, sink, nullptr};
     const auto trampoline = [](odegpu_index it, odegpu_batch*, void* user) -> int {
         auto* x = static_cast<Ctx*>(user);
-        x->batch->invalidate_host(detail::kSolveWrites);
+        x->batch->invalidate_host(kSolveWrites);
         try {
             (*x->sink)(static_cast<Index>(it), static_cast<const SolverBatch&>(*x->batch));
             x->batch->push(); // a sink may not write, but keep the mirror coherent regardless
@@ -90,10 +98,42 @@ void solve_iteratively(SolverBatch& batch, const D& def, const SolverConfig& cfg
         }
     };
     const int rc = odegpu_solve_iteratively(batch.handle(), &m, &c.c_cfg, &c.c_ode, &c.c_ev, iterations,
-                                            +trampoline, &ctx);
-    batch.invalidate_host(detail::kSolveWrites);
+                                            sink ? +trampoline : nullptr, sink ? &ctx : nullptr);
+    batch.invalidate_host(kSolveWrites);
     if (ctx.error) std::rethrow_exception(ctx.error);
-    detail::check(rc);
+    check(rc);
+}
+
+struct NoSink {
+    void operator()(Index, const SolverBatch&) const {}
+};
+
+} // namespace detail
+
+/// Integrates every system of the batch on the GPU (solve.hpp:60-128).
+/// Built-in models run through the C ABI; other SystemModels through a
+/// kernel instantiated from include/odegpu/device/custom.cuh.
+template <SystemModel D>
+void solve(SolverBatch& batch, const D& def, const SolverConfig& cfg = {}) {
+    if constexpr (BuiltinModel<D>)
+        detail::solve_builtin(batch, def, cfg);
+    else
+        solve_custom(batch, def, cfg);
+}
+
+/// solve.hpp:133-142: `iterations` solves, sink(i, const batch&) after each.
+template <SystemModel D, typename Sink>
+void solve_iteratively(SolverBatch& batch, const D& def, const SolverConfig& cfg, Index iterations, Sink&& sink) {
+    if (iterations < 1) throw std::invalid_argument("solve_iteratively: iterations must be >= 1");
+    if constexpr (BuiltinModel<D>) {
+        using S = std::remove_reference_t<Sink>;
+        detail::solve_iteratively_builtin<D, S>(batch, def, cfg, iterations, &sink);
+    } else {
+        for (Index i = 0; i < iterations; ++i) {
+            solve_custom(batch, def, cfg);
+            sink(i, static_cast<const SolverBatch&>(batch));
+        }
+    }
 }
 
 /// Iterations back to back on the device, no host round trip (transient
@@ -101,13 +141,11 @@ void solve_iteratively(SolverBatch& batch, const D& def, const SolverConfig& cfg
 template <SystemModel D>
 void solve_iteratively(SolverBatch& batch, const D& def, const SolverConfig& cfg, Index iterations) {
     if (iterations < 1) throw std::invalid_argument("solve_iteratively: iterations must be >= 1");
-    detail::CControls c(def, cfg);
-    const odegpu_model m = def.descriptor();
-    batch.push();
-    const int rc = odegpu_solve_iteratively(batch.handle(), &m, &c.c_cfg, &c.c_ode, &c.c_ev, iterations, nullptr,
-                                            nullptr);
-    batch.invalidate_host(detail::kSolveWrites);
-    detail::check(rc);
+    if constexpr (BuiltinModel<D>) {
+        detail::solve_iteratively_builtin<D, detail::NoSink>(batch, def, cfg, iterations, nullptr);
+    } else {
+        for (Index i = 0; i < iterations; ++i) solve_custom(batch, def, cfg);
+    }
 }
 
 } // namespace odegpu

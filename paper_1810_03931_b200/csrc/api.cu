@@ -76,8 +76,14 @@ void launch_model(odegpu_batch* b, const odegpu_model& m, int algorithm, const d
 // materialisation into the kernel-parameter struct.
 dev::Controls prepare_solve(const odegpu_batch_dims& d, const odegpu_model* m, const odegpu_solver_config* cfg,
                             const odegpu_ode_controls* ode, const odegpu_event_controls* ev) {
-    if (!m || !cfg || !ode) throw_invalid("solve: null argument");
-    const odegpu_system_dims sys = dims_of(*m);
+    if (!m) throw_invalid("solve: null argument");
+    return validate_solve(d, dims_of(*m), cfg, ode, ev);
+}
+
+dev::Controls validate_solve(const odegpu_batch_dims& d, const odegpu_system_dims& sys,
+                             const odegpu_solver_config* cfg, const odegpu_ode_controls* ode,
+                             const odegpu_event_controls* ev) {
+    if (!cfg || !ode) throw_invalid("solve: null argument");
     if (sys.system_dim != d.system_dim || sys.param_count != d.param_count || sys.event_count != d.event_count ||
         sys.accessory_count != d.accessory_count)
         throw_invalid("solve: definition and batch dimensions disagree");
@@ -92,23 +98,7 @@ dev::Controls prepare_solve(const odegpu_batch_dims& d, const odegpu_model* m, c
     if (sys.event_count > 0 && (!ev || !ev->direction || !ev->tolerance || !ev->stop_condition))
         throw_invalid("solve: event controls missing");
 
-    dev::Controls c{};
-    for (Index i = 0; i < sys.system_dim; ++i) {
-        c.rel_tol[i] = ode->rel_tol[i];
-        c.abs_tol[i] = ode->abs_tol[i];
-    }
-    c.max_step = ode->max_step;
-    c.min_step = ode->min_step;
-    c.step_grow_limit = ode->step_grow_limit;
-    c.step_shrink_limit = ode->step_shrink_limit;
-    c.initial_time_step = cfg->initial_time_step;
-    c.max_steps_in_zone = ev ? ev->max_steps_in_zone : 50;
-    for (Index i = 0; i < sys.event_count; ++i) {
-        c.direction[i] = ev->direction[i];
-        c.tolerance[i] = ev->tolerance[i];
-        c.stop_condition[i] = ev->stop_condition[i];
-    }
-    return c;
+    return dev::controls_from(sys, *cfg, *ode, ev);
 }
 
 void raise_if_bad(odegpu_batch* b) {
@@ -554,6 +544,36 @@ int odegpu_dfma_peak(int device, int blocks, int threads, int iters, double* lan
 }
 
 } // extern "C"
+
+extern "C" int odegpu_custom_begin(odegpu_batch* b, const odegpu_system_dims* dims, const odegpu_solver_config* cfg,
+                                   const odegpu_ode_controls* ode, const odegpu_event_controls* ev,
+                                   odegpu_device_view* view) {
+    return guarded([&] {
+        check_batch(b);
+        if (!dims || !view) throw_invalid("solve: null argument");
+        validate_solve(b->dims, *dims, cfg, ode, ev); // solve.hpp:145-157, same messages
+        DeviceGuard g(b->device);
+        b->a.count = b->dims.batch_capacity;
+        enqueue_time_check(b);
+        CK(cudaMemsetAsync(b->a.work, 0, sizeof(unsigned long long), b->stream));
+        const auto& a = b->a;
+        *view = odegpu_device_view{a.td,          a.state,      a.params,          a.acc,
+                                   a.final_t,     a.reason,     a.accepted,        a.rejected,
+                                   a.detections,  a.secant_failures, a.smallest_step, a.n,
+                                   a.count,       a.work,       b->first_bad,      b->stream,
+                                   b->device,     b->num_sms};
+        ++b->launches; // the caller's solve kernel
+    });
+}
+
+extern "C" int odegpu_custom_end(odegpu_batch* b) {
+    return guarded([&] {
+        check_batch(b);
+        DeviceGuard g(b->device);
+        CK(cudaGetLastError()); // the caller's launch
+        raise_if_bad(b);
+    });
+}
 
 extern "C" int odegpu_math_check(int fn, odegpu_index n, const double* x, const double* y, double* mine,
                                  double* ref) {

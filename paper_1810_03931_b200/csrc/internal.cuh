@@ -125,6 +125,9 @@ odegpu_system_dims dims_of(const odegpu_model& m);
 void launch_model(odegpu_batch* b, const odegpu_model& m, int algorithm, const dev::Controls& c);
 dev::Controls prepare_solve(const odegpu_batch_dims& d, const odegpu_model* m, const odegpu_solver_config* cfg,
                             const odegpu_ode_controls* ode, const odegpu_event_controls* ev);
+dev::Controls validate_solve(const odegpu_batch_dims& d, const odegpu_system_dims& sys,
+                             const odegpu_solver_config* cfg, const odegpu_ode_controls* ode,
+                             const odegpu_event_controls* ev);
 void raise_if_bad(odegpu_batch* b); // syncs the batch stream
 void copy_h2d_strided(Real* dst, Index dst_stride, Index dst_start, const double* src, Index src_stride,
                       Index src_start, Index count, Index components, cudaStream_t s);

@@ -6,15 +6,7 @@
 
 namespace odegpu::detail {
 
-// The skip flag: when the time-domain check found a bad system the solve
-// kernel must not touch anything (the reference throws before solving,
-// solve.hpp:159-161).
-template <class H, Algorithm ALG, int BLOCK, int MINB>
-__global__ void __launch_bounds__(BLOCK, MINB)
-    guarded_solve_kernel(H model, dev::BatchArrays b, dev::Controls c, const unsigned long long* first_bad) {
-    if (*first_bad != ~0ull) return;
-    dev::solve_lanes<H, ALG, BLOCK>(model, b, c);
-}
+using dev::guarded_solve_kernel;
 
 /// Per-model launch policy: resident blocks of kBlock threads per SM that
 /// __launch_bounds__ asks ptxas for (register cap 65536 / (kMinBlocks *

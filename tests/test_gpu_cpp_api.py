@@ -11,10 +11,16 @@ BIN = ROOT / "build" / "cpp" / "test_host_api"
 
 
 @pytest.mark.gpu
-def test_cpp_host_api_suite():
-    if not BIN.exists():
+@pytest.mark.parametrize("name", ["test_host_api", "test_custom_model"])
+def test_cpp_suite(name):
+    """test_host_api: the reference's batch/driver/scan cases on the C++ API;
+    test_custom_model: user-defined SystemModels compiled by nvcc through
+    include/odegpu/device/custom.cuh (a clone of a built-in model must match
+    it bitwise)."""
+    binary = ROOT / "build" / "cpp" / name
+    if not binary.exists():
         subprocess.run(["make", "-C", str(ROOT), "cpptests"], check=True)
-    r = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([str(binary)], capture_output=True, text=True, timeout=600)
     print(r.stdout[-4000:])
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert ", 0 failed" in r.stdout
