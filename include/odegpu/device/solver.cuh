@@ -21,6 +21,7 @@
 
 #include <cstdint>
 #include <span>
+#include <type_traits>
 
 #include "odegpu.h"
 #include "odegpu/device/dmath.cuh"
@@ -282,8 +283,13 @@ __device__ __forceinline__ bool rk_step(const H& m, Real t, Real h, const Real (
     return !finite;
 }
 
-// Event zones (events.hpp:22-26) and transitions (events.hpp:54-70).
-enum : int { kZoneNone = -1, kZoneBelow = 0, kZoneInside = 1, kZoneAbove = 2 };
+// Event zones (events.hpp:22-26) and transitions (events.hpp:54-70). Zone
+// codes fit two bits so a lane keeps zone_of(prev_value) of every event in
+// one register. EventMachine's phase is implied: an event is Leaving exactly
+// when its previous value sits inside the zone (init, events.hpp:93-101, and
+// refresh, events.hpp:160-173, set both together), and classify_transition
+// never fires from Inside, so the phase needs no storage of its own.
+enum : int { kZoneBelow = 0, kZoneInside = 1, kZoneAbove = 2, kZoneNone = 3 };
 enum : int { kKindNone = -1, kKindAcross = 0, kKindEntered = 1 };
 
 __device__ __forceinline__ int zone_of(Real v, Real tol) {
@@ -292,19 +298,23 @@ __device__ __forceinline__ int zone_of(Real v, Real tol) {
     return v > 0 ? kZoneAbove : kZoneBelow;
 }
 
-/// classify_transition with phase Normal folded in by the caller.
+/// classify_transition (events.hpp:54-70) from the previous zone; kZoneNone
+/// on either side and Inside before (phase Leaving) give no detection.
 __device__ __forceinline__ int classify(int prev, int next, int direction) {
-    if (prev == kZoneAbove) {
-        if (next == kZoneBelow && direction <= 0) return kKindAcross;
-        if (next == kZoneInside && direction <= 0) return kKindEntered;
-        return kKindNone;
+    if (prev == kZoneAbove && direction <= 0) {
+        if (next == kZoneBelow) return kKindAcross;
+        if (next == kZoneInside) return kKindEntered;
     }
-    if (prev == kZoneBelow) {
-        if (next == kZoneAbove && direction >= 0) return kKindAcross;
-        if (next == kZoneInside && direction >= 0) return kKindEntered;
-        return kKindNone;
+    if (prev == kZoneBelow && direction >= 0) {
+        if (next == kZoneAbove) return kKindAcross;
+        if (next == kZoneInside) return kKindEntered;
     }
     return kKindNone;
+}
+
+__device__ __forceinline__ int zone_at(int zones, int i) { return (zones >> (2 * i)) & 3; }
+__device__ __forceinline__ int with_zone(int zones, int i, int z) {
+    return (zones & ~(3 << (2 * i))) | (z << (2 * i));
 }
 
 /// Hands out the next system index; lanes arriving together share one
@@ -318,16 +328,20 @@ __device__ __forceinline__ Index fetch_system(unsigned long long* work) {
     return static_cast<Index>(base + g.thread_rank());
 }
 
-
-enum Phase : int { kFetch = 0, kStep = 1, kSecant = 2, kCommit = 3, kFinish = 4, kDone = 5 };
+/// Lane phases. Those below kReadyStep are bookkeeping run in the prepare
+/// loop; kReadyStep / kReadySecant mean an RK evaluation of length h_step
+/// from (t, y) is pending (a trial step, or one secant re-step).
+enum Phase : int {
+    kFetch = 0, kSetup = 1, kSecant = 2, kCommit = 3, kFinish = 4, kDone = 5, kReadyStep = 6, kReadySecant = 7
+};
 
 constexpr int kMaxSecantIterations = 50; // events.hpp:190
 
-/// Cold per-lane state of the state machine: everything that is not needed
-/// inside the Runge-Kutta stages. It lives in shared memory as structure of
-/// arrays (one column per thread, bank-conflict free) so that only the hot
-/// set — t, h, y and the stage vectors — occupies registers during the
-/// stages; that is what sets occupancy (SURVEY.md §8d register table).
+/// Cold per-lane state: what only the infrequent paths touch (system
+/// entry/exit, detections, the secant, accessories). It lives in shared
+/// memory as structure of arrays (one column per thread, bank-conflict free)
+/// so that only the hot set — t, h, y, the step bookkeeping and the stage
+/// vectors — occupies registers; that is what sets occupancy.
 template <class H, int BLOCK>
 struct ColdState {
     static constexpr int N = H::kSystemDim;
@@ -338,14 +352,21 @@ struct ColdState {
     Real y_land[N][BLOCK];
     Real f_land[E][BLOCK];
     Real prev_value[E][BLOCK]; // EventMachine (events.hpp:76-178)
-    Real t1[BLOCK], h[BLOCK], h_try[BLOCK], h_next[BLOCK], t_land[BLOCK], smallest[BLOCK];
+    Real h_try[BLOCK], h_next[BLOCK], t_land[BLOCK];
     Real th_prev[BLOCK], f_prev[BLOCK], th_cur[BLOCK], f_cur[BLOCK], th_min[BLOCK], b_th[BLOCK], b_f[BLOCK];
     long long sys[BLOCK];
-    unsigned n_acc[BLOCK], n_rej[BLOCK], n_det[BLOCK], n_secf[BLOCK];
+    unsigned n_det[BLOCK], n_secf[BLOCK];
     int counter[E][BLOCK];
-    int steps_in_zone[BLOCK], s_it[BLOCK], s_idx[BLOCK], located[BLOCK];
-    unsigned char leaving[E][BLOCK], clipped[BLOCK], relocated[BLOCK], s_conv[BLOCK], reason[BLOCK];
+    int s_it[BLOCK], s_idx[BLOCK], located[BLOCK];
+    unsigned char clipped[BLOCK], relocated[BLOCK], s_conv[BLOCK], reason[BLOCK];
 };
+
+/// Whether a model overrides a HookDefaults no-op (inherited hooks keep the
+/// HookDefaults member-pointer type): per-step hooks that do nothing cost
+/// nothing, not even the shared-memory traffic around them.
+template <class H>
+inline constexpr bool kHasOrdinaryAccessory = !std::is_same_v<decltype(&H::ordinary_accessory),
+                                                              decltype(&HookDefaults::ordinary_accessory)>;
 
 /// Per-model kernel structure, chosen from ncu measurements
 /// and specialisable for custom models:
@@ -385,13 +406,23 @@ struct EffectivePolicy {
 };
 
 /// The ensemble loop. One instantiation per (model, algorithm): hooks are
-/// inlined, widths are compile-time; hot state in registers, cold state in
-/// shared memory.
+/// inlined, widths are compile-time.
+///
+/// Each iteration: (1) PREPARE — lanes without a pending RK evaluation run
+/// their bookkeeping (fetch + initialize a system, commit a detection step,
+/// finalize + store, the secant update); (2) every lane evaluates one RK
+/// step; (3) ABSORB — error control, and for the common outcome (rejected,
+/// or accepted without an event detection) the whole of driver.hpp:146-227
+/// inline in registers: landing, refresh of the event zones, accessories,
+/// the next step's clipping — so a lane is ready for its next evaluation
+/// without another trip through the state machine. Only detections, stops
+/// and system ends go back through PREPARE.
 template <class H, Algorithm ALG, int BLOCK>
 __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, const Controls& c) {
     constexpr int N = H::kSystemDim;
     constexpr int NP = H::kParamCount, NA = H::kAccessoryCount, E = H::kEventCount;
     constexpr int EE = E > 0 ? E : 1, A = NA > 0 ? NA : 1;
+    constexpr bool kAdaptive = ALG == Algorithm::RKCK45;
     using Pol = EffectivePolicy<H>;
     static_assert(N <= kMaxDim && E <= kMaxEvents, "model wider than the device controls");
     constexpr bool kFence = Pol::kColdInShared || Pol::kParamsInShared;
@@ -413,15 +444,18 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
     const auto CS = [](const Real* a, int len) { return std::span<const Real>(a, static_cast<std::size_t>(len)); };
 #define ODEGPU_C(field) cs.field[tid]
 
-    // ---- hot registers
-    Real t = 0, h_step = 0;
+    // ---- hot registers: the driver's loop variables (driver.hpp:96-107)
+    Real t = 0, t1 = 0, h = 0, h_step = 0;
+    Real smallest = 0;               // SystemOutcome::smallest_step
     Real y[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) y[i] = 0;
+    unsigned n_acc = 0, n_rej = 0;   // accepted / rejected steps
+    int zones = 0;                   // zone_of(prev_value[i]), 2 bits per event
+    int steps_in_zone = 0;           // EventMachine::steps_in_zone_
+    bool clipped = false;
     int phase = kFetch;
 
-    // Helpers moving the small hook arguments between shared memory and
-    // register arrays around (infrequent) hook calls.
     const auto load_acc = [&](Real (&a)[A]) {
 #pragma unroll
         for (int i = 0; i < A; ++i) a[i] = ODEGPU_C(acc[i]);
@@ -430,28 +464,59 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
 #pragma unroll
         for (int i = 0; i < NA; ++i) ODEGPU_C(acc[i]) = a[i];
     };
-    const auto landed_values = [&](Real tt) { // F at the landed point -> f_land
-        Real yl[N], f[EE];
+    // driver.hpp:109-119: clip the next trial step onto t1; false when the
+    // system is done (the lane goes to kFinish).
+    const auto setup_step = [&]() {
+        if (!(t < t1)) {
+            phase = kFinish;
+            return;
+        }
+        Real h_try = h;
+        clipped = false;
+        if (t + h_try >= t1) {
+            h_try = t1 - t;
+            clipped = true;
+        }
+        if (!(h_try > 0)) { // fp underflow of the remaining span
+            t = t1;
+            phase = kFinish;
+            return;
+        }
+        h_step = h_try;
+        phase = kReadyStep;
+    };
+    // EventMachine::refresh (events.hpp:160-173) from post-action values.
+    const auto refresh = [&](const Real (&fp)[EE]) {
+        bool any_inside = false;
 #pragma unroll
-        for (int i = 0; i < N; ++i) yl[i] = ODEGPU_C(y_land[i]);
-        m.event_values(tt, CS(yl, N), CS(prow, NP), S(f, E));
-#pragma unroll
-        for (int i = 0; i < E; ++i) ODEGPU_C(f_land[i]) = f[i];
+        for (int i = 0; i < E; ++i) {
+            const int z = zone_of(fp[i], c.tolerance[i]);
+            if (z == kZoneNone) continue; // non-finite: keep the previous arming
+            ODEGPU_C(prev_value[i]) = fp[i];
+            zones = with_zone(zones, i, z);
+            any_inside = any_inside || z == kZoneInside;
+        }
+        steps_in_zone = any_inside ? steps_in_zone + 1 : 0;
     };
     // Ends a secant location (driver.hpp:157-164).
     const auto end_secant = [&]() {
         if (!ODEGPU_C(s_conv)) ++ODEGPU_C(n_secf);
         const bool rel = ODEGPU_C(b_th) < ODEGPU_C(h_try);
         ODEGPU_C(relocated) = rel;
-        const Real tl = (ODEGPU_C(clipped) && !rel) ? ODEGPU_C(t1) : t + ODEGPU_C(b_th);
+        const Real tl = (ODEGPU_C(clipped) && !rel) ? t1 : t + ODEGPU_C(b_th);
         ODEGPU_C(t_land) = tl;
-        landed_values(tl);
+        Real yl[N], f[EE];
+#pragma unroll
+        for (int i = 0; i < N; ++i) yl[i] = ODEGPU_C(y_land[i]);
+        m.event_values(tl, CS(yl, N), CS(prow, NP), S(f, E));
+#pragma unroll
+        for (int i = 0; i < E; ++i) ODEGPU_C(f_land[i]) = f[i];
         phase = kCommit;
     };
 
     for (;;) {
         // ================= PREPARE: bring this lane to a pending RK evaluation
-        for (;;) {
+        while (phase < kDone) {
             if (phase == kFetch) {
                 const Index sys = fetch_system(b.work);
                 if (sys >= b.count) {
@@ -468,8 +533,9 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 Real acc[A];
 #pragma unroll
                 for (int i = 0; i < NA; ++i) acc[i] = b.acc[sys + i * n];
-                ODEGPU_C(n_acc) = ODEGPU_C(n_rej) = ODEGPU_C(n_det) = ODEGPU_C(n_secf) = 0u;
-                ODEGPU_C(smallest) = __longlong_as_double(0x7ff0000000000000LL); // +inf
+                n_acc = n_rej = 0u;
+                ODEGPU_C(n_det) = ODEGPU_C(n_secf) = 0u;
+                smallest = __longlong_as_double(0x7ff0000000000000LL); // +inf
                 ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::ReachedEndTime);
                 // driver.hpp:96-107
                 m.initialize(td[0], S(td, 2), S(y, N), CS(prow, NP), S(acc, NA));
@@ -477,94 +543,87 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 ODEGPU_C(td[1]) = td[1];
                 store_acc(acc);
                 t = td[0];
-                ODEGPU_C(t1) = td[1];
-                if constexpr (E > 0) {
+                t1 = td[1];
+                if constexpr (E > 0) { // EventMachine::init (events.hpp:93-101)
                     Real f0[EE];
                     m.event_values(t, CS(y, N), CS(prow, NP), S(f0, E));
+                    zones = 0;
 #pragma unroll
                     for (int i = 0; i < E; ++i) {
                         ODEGPU_C(prev_value[i]) = f0[i];
-                        ODEGPU_C(leaving[i]) = zone_of(f0[i], c.tolerance[i]) == kZoneInside;
+                        zones = with_zone(zones, i, zone_of(f0[i], c.tolerance[i]));
                         ODEGPU_C(counter[i]) = 0;
                     }
-                    ODEGPU_C(steps_in_zone) = 0;
+                    steps_in_zone = 0;
                 }
-                ODEGPU_C(h) = ALG == Algorithm::RK4 ? c.initial_time_step
-                                                    : sclamp(c.initial_time_step, c.min_step, c.max_step);
-                phase = kStep;
+                h = kAdaptive ? sclamp(c.initial_time_step, c.min_step, c.max_step) : c.initial_time_step;
+                phase = kSetup;
+            }
+            if (phase == kSetup) {
+                setup_step();
+                continue;
             }
             if (phase == kCommit) {
-                // driver.hpp:170-227
+                // an accepted step with a detection: driver.hpp:170-227
                 const Real tl = ODEGPU_C(t_land);
                 if (tl <= t) {
                     ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::NonFiniteAbort);
                     phase = kFinish;
-                } else {
-                    const Real advanced = tl - t;
-#pragma unroll
-                    for (int i = 0; i < N; ++i) y[i] = ODEGPU_C(y_land[i]);
-                    t = tl;
-                    ++ODEGPU_C(n_acc);
-                    ODEGPU_C(smallest) = smin(ODEGPU_C(smallest), advanced);
-                    bool event_stop = false;
-                    Real acc[A];
-                    load_acc(acc);
-                    if constexpr (E > 0) {
-                        const int located = ODEGPU_C(located);
-                        bool det[EE];
-                        int cnt[EE];
-#pragma unroll
-                        for (int i = 0; i < E; ++i) { // EventMachine::commit, events.hpp:134-156
-                            const Real fl = ODEGPU_C(f_land[i]);
-                            const int pz = zone_of(ODEGPU_C(prev_value[i]), c.tolerance[i]);
-                            const int nz = zone_of(fl, c.tolerance[i]);
-                            const bool kind = pz != kZoneNone && nz != kZoneNone && !ODEGPU_C(leaving[i]) &&
-                                              classify(pz, nz, c.direction[i]) != kKindNone;
-                            det[i] = kind || i == located;
-                            cnt[i] = ODEGPU_C(counter[i]) + (det[i] ? 1 : 0);
-                            ODEGPU_C(counter[i]) = cnt[i];
-                            if (det[i]) ++ODEGPU_C(n_det);
-                        }
-                        Real f_post[EE];
-                        if (located >= 0) {
-#pragma unroll
-                            for (int i = 0; i < E; ++i)
-                                if (i == located) m.event_action(i, cnt[i], t, S(y, N), CS(prow, NP));
-                            m.event_values(t, CS(y, N), CS(prow, NP), S(f_post, E));
-                        } else {
-#pragma unroll
-                            for (int i = 0; i < E; ++i) f_post[i] = ODEGPU_C(f_land[i]);
-                        }
-                        bool any_inside = false; // EventMachine::refresh, events.hpp:160-173
-#pragma unroll
-                        for (int i = 0; i < E; ++i) {
-                            const int z = zone_of(f_post[i], c.tolerance[i]);
-                            if (z == kZoneNone) continue;
-                            ODEGPU_C(prev_value[i]) = f_post[i];
-                            ODEGPU_C(leaving[i]) = z == kZoneInside;
-                            any_inside = any_inside || z == kZoneInside;
-                        }
-                        ODEGPU_C(steps_in_zone) = any_inside ? ODEGPU_C(steps_in_zone) + 1 : 0;
-#pragma unroll
-                        for (int i = 0; i < E; ++i)
-                            if (det[i]) m.event_accessory(i, cnt[i], t, CS(y, N), CS(prow, NP), S(acc, NA));
-#pragma unroll
-                        for (int i = 0; i < E; ++i)
-                            if (det[i] && c.stop_condition[i] != 0 && cnt[i] >= c.stop_condition[i]) event_stop = true;
-                    }
-                    m.ordinary_accessory(t, CS(y, N), CS(prow, NP), S(acc, NA));
-                    store_acc(acc);
-                    if (event_stop) {
-                        ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::EventStop);
-                        phase = kFinish;
-                    } else if (E > 0 && ODEGPU_C(steps_in_zone) >= c.max_steps_in_zone) {
-                        ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::EquilibriumStop);
-                        phase = kFinish;
-                    } else {
-                        if (ALG == Algorithm::RKCK45 && !ODEGPU_C(relocated)) ODEGPU_C(h) = ODEGPU_C(h_next);
-                        phase = kStep;
-                    }
+                    continue;
                 }
+                const Real advanced = tl - t;
+#pragma unroll
+                for (int i = 0; i < N; ++i) y[i] = ODEGPU_C(y_land[i]);
+                t = tl;
+                ++n_acc;
+                smallest = smin(smallest, advanced);
+                bool event_stop = false;
+                Real acc[A];
+                load_acc(acc);
+                if constexpr (E > 0) {
+                    const int located = ODEGPU_C(located);
+                    bool det[EE];
+                    int cnt[EE];
+#pragma unroll
+                    for (int i = 0; i < E; ++i) { // EventMachine::commit, events.hpp:134-156
+                        const int kind = classify(zone_at(zones, i), zone_of(ODEGPU_C(f_land[i]), c.tolerance[i]),
+                                                  c.direction[i]);
+                        det[i] = kind != kKindNone || i == located;
+                        cnt[i] = ODEGPU_C(counter[i]) + (det[i] ? 1 : 0);
+                        ODEGPU_C(counter[i]) = cnt[i];
+                        if (det[i]) ++ODEGPU_C(n_det);
+                    }
+                    Real f_post[EE];
+                    if (located >= 0) {
+#pragma unroll
+                        for (int i = 0; i < E; ++i)
+                            if (i == located) m.event_action(i, cnt[i], t, S(y, N), CS(prow, NP));
+                        m.event_values(t, CS(y, N), CS(prow, NP), S(f_post, E));
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < E; ++i) f_post[i] = ODEGPU_C(f_land[i]);
+                    }
+                    refresh(f_post);
+#pragma unroll
+                    for (int i = 0; i < E; ++i)
+                        if (det[i]) m.event_accessory(i, cnt[i], t, CS(y, N), CS(prow, NP), S(acc, NA));
+#pragma unroll
+                    for (int i = 0; i < E; ++i)
+                        if (det[i] && c.stop_condition[i] != 0 && cnt[i] >= c.stop_condition[i]) event_stop = true;
+                }
+                m.ordinary_accessory(t, CS(y, N), CS(prow, NP), S(acc, NA));
+                store_acc(acc);
+                if (event_stop) {
+                    ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::EventStop);
+                    phase = kFinish;
+                } else if (E > 0 && steps_in_zone >= c.max_steps_in_zone) {
+                    ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::EquilibriumStop);
+                    phase = kFinish;
+                } else {
+                    if (kAdaptive && !ODEGPU_C(relocated)) h = ODEGPU_C(h_next);
+                    setup_step();
+                }
+                continue;
             }
             if (phase == kFinish) {
                 // driver.hpp:231-233, then scatter_system (batch.cpp:32-40)
@@ -581,36 +640,13 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 for (int i = 0; i < NA; ++i) b.acc[sys + i * n] = acc[i];
                 b.final_t[sys] = t;
                 b.reason[sys] = ODEGPU_C(reason);
-                b.accepted[sys] = ODEGPU_C(n_acc);
-                b.rejected[sys] = ODEGPU_C(n_rej);
+                b.accepted[sys] = n_acc;
+                b.rejected[sys] = n_rej;
                 b.detections[sys] = ODEGPU_C(n_det);
                 b.secant_failures[sys] = ODEGPU_C(n_secf);
-                b.smallest_step[sys] = ODEGPU_C(smallest);
+                b.smallest_step[sys] = smallest;
                 phase = kFetch;
                 continue;
-            }
-            if (phase == kStep) {
-                // driver.hpp:109-119
-                const Real t1 = ODEGPU_C(t1);
-                if (!(t < t1)) {
-                    phase = kFinish;
-                    continue;
-                }
-                Real h_try = ODEGPU_C(h);
-                bool clipped = false;
-                if (t + h_try >= t1) {
-                    h_try = t1 - t;
-                    clipped = true;
-                }
-                if (!(h_try > 0)) {
-                    t = t1;
-                    phase = kFinish;
-                    continue;
-                }
-                ODEGPU_C(h_try) = h_try;
-                ODEGPU_C(clipped) = clipped;
-                h_step = h_try;
-                break;
             }
             if (phase == kSecant) {
                 // events.hpp:214-219: the pre-step exits of one secant iteration
@@ -635,10 +671,14 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     continue;
                 }
                 h_step = theta;
-                break;
+                phase = kReadySecant;
             }
         }
-        if (phase == kDone) break;
+        // Warp-uniform exit: every lane stays resident until its whole warp
+        // is done, and the vote re-converges the warp, so the RK stages below
+        // always run once per iteration for all lanes (finished lanes compute
+        // on stale state and ignore the result).
+        if (__all_sync(0xffffffffu, phase == kDone)) break;
 
         // ================= the shared Runge-Kutta evaluation
         if constexpr (kFence) cold_fence();
@@ -647,16 +687,15 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
         if constexpr (kFence) cold_fence();
 
         // ================= ABSORB
-        if (phase == kStep) {
+        if (phase == kReadyStep) {
             const Real h_try = h_step;
-            Real h_next;
-            if constexpr (ALG == Algorithm::RK4) {
+            Real h_next = h;
+            if constexpr (!kAdaptive) {
                 if (nonfinite) { // driver.hpp:124-128
                     ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::NonFiniteAbort);
                     phase = kFinish;
                     continue;
                 }
-                h_next = ODEGPU_C(h);
             } else {
                 // error_ratio (steppers.hpp:154-163) + control_step (176-198)
                 Real ratio = 0.0;
@@ -676,7 +715,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     h_next = smax(h_try * c.step_shrink_limit, c.min_step);
                 } else {
                     accepted = ratio <= 1.0;
-                    Real factor = 0.9 * dmath::pow(ratio, -0.2);
+                    Real factor = 0.9 * dmath::pow_neg_fifth(ratio); // std::pow(ratio, -0.2)
                     factor = sclamp(factor, c.step_shrink_limit, c.step_grow_limit);
                     h_next = sclamp(h_try * factor, c.min_step, c.max_step);
                     if (!accepted && h_try <= c.min_step) {
@@ -684,64 +723,96 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                         h_next = c.min_step;
                     }
                 }
-                if (!accepted) {
-                    ++ODEGPU_C(n_rej);
-                    ODEGPU_C(h) = h_next;
+                if (!accepted) { // driver.hpp:136-140; t < t1 still holds
+                    ++n_rej;
+                    h = h_next;
+                    setup_step();
                     continue;
                 }
             }
-            ODEGPU_C(h_next) = h_next;
             // accepted: driver.hpp:146-168
-            const Real tl = ODEGPU_C(clipped) ? ODEGPU_C(t1) : t + h_try;
-            ODEGPU_C(t_land) = tl;
-#pragma unroll
-            for (int i = 0; i < N; ++i) ODEGPU_C(y_land[i]) = yn[i];
-            int located = -1;
-            ODEGPU_C(relocated) = false;
-            phase = kCommit;
+            const Real tl = clipped ? t1 : t + h_try;
             if constexpr (E > 0) {
                 Real f[EE];
                 m.event_values(tl, CS(yn, N), CS(prow, NP), S(f, E));
-#pragma unroll
-                for (int i = 0; i < E; ++i) ODEGPU_C(f_land[i]) = f[i];
                 // EventMachine::peek (events.hpp:111-125): highest index wins
-                bool needs = false;
+                int located = -1, kind = kKindNone;
 #pragma unroll
                 for (int i = E - 1; i >= 0; --i) {
                     if (located >= 0) break;
-                    const int pz = zone_of(ODEGPU_C(prev_value[i]), c.tolerance[i]);
-                    const int nz = zone_of(f[i], c.tolerance[i]);
-                    if (pz == kZoneNone || nz == kZoneNone || ODEGPU_C(leaving[i])) continue;
-                    const int kind = classify(pz, nz, c.direction[i]);
-                    if (kind != kKindNone) {
+                    const int k = classify(zone_at(zones, i), zone_of(f[i], c.tolerance[i]), c.direction[i]);
+                    if (k != kKindNone) {
                         located = i;
-                        needs = kind == kKindAcross;
+                        kind = k;
                     }
                 }
-                if (located >= 0 && needs) {
-                    // start locate_secant (events.hpp:207-212); y_land holds y(h)
-                    ODEGPU_C(s_idx) = located;
-                    ODEGPU_C(s_it) = 1;
-                    ODEGPU_C(s_conv) = false;
-                    ODEGPU_C(th_prev) = 0;
-                    ODEGPU_C(th_cur) = h_try;
-                    ODEGPU_C(th_min) = h_try * 1e-12;
-                    Real fp = 0, fc = 0;
+                if (located >= 0) { // detection: the slow path through PREPARE
+                    ODEGPU_C(t_land) = tl;
 #pragma unroll
-                    for (int i = 0; i < E; ++i)
-                        if (i == located) {
-                            fp = ODEGPU_C(prev_value[i]);
-                            fc = f[i];
-                        }
-                    ODEGPU_C(f_prev) = fp;
-                    ODEGPU_C(f_cur) = fc;
-                    ODEGPU_C(b_th) = h_try;
-                    ODEGPU_C(b_f) = fc;
-                    phase = kSecant;
+                    for (int i = 0; i < N; ++i) ODEGPU_C(y_land[i]) = yn[i];
+#pragma unroll
+                    for (int i = 0; i < E; ++i) ODEGPU_C(f_land[i]) = f[i];
+                    ODEGPU_C(h_next) = h_next;
+                    ODEGPU_C(located) = located;
+                    ODEGPU_C(relocated) = false;
+                    phase = kCommit;
+                    if (kind == kKindAcross) {
+                        // start locate_secant (events.hpp:207-212); y_land holds y(h)
+                        ODEGPU_C(h_try) = h_try;
+                        ODEGPU_C(clipped) = clipped;
+                        ODEGPU_C(s_idx) = located;
+                        ODEGPU_C(s_it) = 1;
+                        ODEGPU_C(s_conv) = false;
+                        ODEGPU_C(th_prev) = 0;
+                        ODEGPU_C(th_cur) = h_try;
+                        ODEGPU_C(th_min) = h_try * 1e-12;
+                        Real fp = 0, fc = 0;
+#pragma unroll
+                        for (int i = 0; i < E; ++i)
+                            if (i == located) {
+                                fp = ODEGPU_C(prev_value[i]);
+                                fc = f[i];
+                            }
+                        ODEGPU_C(f_prev) = fp;
+                        ODEGPU_C(f_cur) = fc;
+                        ODEGPU_C(b_th) = h_try;
+                        ODEGPU_C(b_f) = fc;
+                        phase = kSecant;
+                    }
+                    continue;
+                }
+                if (tl <= t) { // driver.hpp:170-173
+                    ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::NonFiniteAbort);
+                    phase = kFinish;
+                    continue;
+                }
+                refresh(f); // no detection: commit records nothing, f_post = f_landed
+            } else {
+                if (tl <= t) {
+                    ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::NonFiniteAbort);
+                    phase = kFinish;
+                    continue;
                 }
             }
-            ODEGPU_C(located) = located;
-        } else { // kSecant: one secant iteration's step is in (events.hpp:222-240)
+            smallest = smin(smallest, tl - t);
+#pragma unroll
+            for (int i = 0; i < N; ++i) y[i] = yn[i];
+            t = tl;
+            ++n_acc;
+            if constexpr (kHasOrdinaryAccessory<H>) {
+                Real acc[A];
+                load_acc(acc);
+                m.ordinary_accessory(t, CS(y, N), CS(prow, NP), S(acc, NA));
+                store_acc(acc);
+            }
+            if (E > 0 && steps_in_zone >= c.max_steps_in_zone) {
+                ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::EquilibriumStop);
+                phase = kFinish;
+                continue;
+            }
+            h = h_next;
+            setup_step();
+        } else if (phase == kReadySecant) { // one secant iteration's step is in (events.hpp:222-240)
             if constexpr (E > 0) {
                 Real fs[EE];
                 m.event_values(t + h_step, CS(yn, N), CS(prow, NP), S(fs, E));
@@ -774,6 +845,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 ODEGPU_C(th_cur) = h_step;
                 ODEGPU_C(f_cur) = f;
                 ++ODEGPU_C(s_it);
+                phase = kSecant;
             }
         }
     }

@@ -9,6 +9,9 @@
 
 #include "odegpu/hooks.hpp"
 #include "odegpu/system.hpp"
+#if defined(__CUDACC__)
+#include "odegpu/device/dmath.cuh"
+#endif
 
 namespace odegpu::models {
 
@@ -18,7 +21,12 @@ ODEGPU_HD ODEGPU_INLINE void duffing_rhs(Real t, std::span<const Real> y, std::s
                                          std::span<Real> dy) {
     const Real k = p[0], B = p[1], delta = p[2], omega = p[3];
     dy[0] = y[1];
-    dy[1] = delta * y[0] - y[0] * y[0] * y[0] - k * y[1] + B * cos(omega * t);
+#if defined(__CUDA_ARCH__)
+    const Real c = device::dmath::cos(omega * t); // == ::cos, bitwise (dmath.cuh)
+#else
+    const Real c = std::cos(omega * t);
+#endif
+    dy[1] = delta * y[0] - y[0] * y[0] * y[0] - k * y[1] + B * c;
 }
 
 /// Duffing + linearised radius/angle (duffing.hpp:47-57).
@@ -30,7 +38,7 @@ ODEGPU_HD ODEGPU_INLINE void duffing_lyapunov_rhs(Real t, std::span<const Real> 
     const Real g2 = -k;
     Real s, c;
 #if defined(__CUDA_ARCH__)
-    sincos(y[3], &s, &c);
+    device::dmath::sincos_fast(y[3], &s, &c);
 #else
     s = std::sin(y[3]);
     c = std::cos(y[3]);

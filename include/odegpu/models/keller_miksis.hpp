@@ -36,8 +36,8 @@ ODEGPU_HD ODEGPU_INLINE void keller_miksis_rhs(Real tau, std::span<const Real> y
     const Real arg2 = two_pi * c[11] * tau + c[12];
     Real s1, c1, s2, c2;
 #if defined(__CUDA_ARCH__)
-    device::dmath::sincos(arg1, &s1, &c1);
-    device::dmath::sincos(arg2, &s2, &c2);
+    device::dmath::sincos_fast(arg1, &s1, &c1);
+    device::dmath::sincos_fast(arg2, &s2, &c2);
 #else
     s1 = std::sin(arg1);
     c1 = std::cos(arg1);

@@ -12,6 +12,14 @@ using dev::guarded_solve_kernel;
 /// __launch_bounds__ asks ptxas for (register cap 65536 / (kMinBlocks *
 /// kBlock)). Chosen per model family from ncu runs;
 /// ODEGPU_MIN_BLOCKS overrides it for tuning builds.
+/// ODEGPU_MB(x): a model's chosen minimum resident blocks, unless a tuning
+/// build forces one value for every model (-DODEGPU_MIN_BLOCKS).
+#ifdef ODEGPU_MIN_BLOCKS
+#define ODEGPU_MB(x) ODEGPU_MIN_BLOCKS
+#else
+#define ODEGPU_MB(x) (x)
+#endif
+
 template <class H>
 struct LaunchPolicy {
 #ifdef ODEGPU_MIN_BLOCKS

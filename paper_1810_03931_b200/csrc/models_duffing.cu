@@ -20,24 +20,24 @@ namespace odegpu::detail {
 //   enough registers (123 -> 72) for 7 blocks of 128 threads per SM.
 template <>
 struct LaunchPolicy<models::DuffingMaxMinHooks> {
-    static constexpr int kMinBlocks = 1;
+    static constexpr int kMinBlocks = ODEGPU_MB(1);
 };
 template <>
 struct LaunchPolicy<models::DuffingMaxEventHooks> {
-    static constexpr int kMinBlocks = 7;
+    static constexpr int kMinBlocks = ODEGPU_MB(7);
 };
 template <>
 struct LaunchPolicy<models::DuffingMaxAccessoryHooks> {
-    static constexpr int kMinBlocks = 7;
+    static constexpr int kMinBlocks = ODEGPU_MB(7);
 };
 template <>
 struct LaunchPolicy<models::DuffingHooks> {
-    static constexpr int kMinBlocks = 7;
+    static constexpr int kMinBlocks = ODEGPU_MB(7);
 };
 // 4-dim Lyapunov system: 3 blocks/SM (<= 168 regs) keeps it spill-free.
 template <>
 struct LaunchPolicy<models::DuffingLyapunovHooks> {
-    static constexpr int kMinBlocks = 3;
+    static constexpr int kMinBlocks = ODEGPU_MB(3);
 };
 
 bool family_dims_duffing(const odegpu_model& m, odegpu_system_dims* d) {

@@ -11,7 +11,7 @@ namespace odegpu::detail {
 // tableau).
 template <>
 struct LaunchPolicy<models::ValveHooks> {
-    static constexpr int kMinBlocks = 6;
+    static constexpr int kMinBlocks = ODEGPU_MB(6);
 };
 
 bool family_dims_valve(const odegpu_model& m, odegpu_system_dims* d) {

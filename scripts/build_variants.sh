@@ -1,6 +1,6 @@
 #!/bin/bash
 # Tuning builds of libodegpu with forced kernel-structure policies:
-#   scripts/build_variants.sh name:ROLLED:COLD_SHARED:PARAMS_SHARED:MIN_BLOCKS ...
+#   scripts/build_variants.sh name:ROLLED:COLD_SHARED:PARAMS_SHARED:MIN_BLOCKS ...  ('-' keeps the model's own)
 # -> paper_1810_03931_b200/lib/variants/libodegpu_<name>.so (load with ODEGPU_LIB=...)
 set -e
 cd "$(dirname "$0")/.."
@@ -9,7 +9,11 @@ mkdir -p paper_1810_03931_b200/lib/variants build/variants
 for spec in "$@"; do
   IFS=: read name rolled cold params mb <<< "$spec"
   od=build/variants/$name; mkdir -p $od
-  defs="-DODEGPU_POLICY_ROLLED=$rolled -DODEGPU_POLICY_COLD_SHARED=$cold -DODEGPU_POLICY_PARAMS_SHARED=$params -DODEGPU_MIN_BLOCKS=$mb"
+  defs=""
+  [ "$rolled" != "-" ] && defs="$defs -DODEGPU_POLICY_ROLLED=$rolled"
+  [ "$cold" != "-" ] && defs="$defs -DODEGPU_POLICY_COLD_SHARED=$cold"
+  [ "$params" != "-" ] && defs="$defs -DODEGPU_POLICY_PARAMS_SHARED=$params"
+  [ "$mb" != "-" ] && defs="$defs -DODEGPU_MIN_BLOCKS=$mb"
   for f in paper_1810_03931_b200/csrc/*.cu; do
     b=$(basename $f .cu)
     nvcc $NVFLAGS $defs -Xptxas -v -c -o $od/$b.o $f 2> $od/$b.ptxas &
