@@ -361,6 +361,17 @@ struct ColdState {
     unsigned char clipped[BLOCK], relocated[BLOCK], s_conv[BLOCK], reason[BLOCK];
 };
 
+/// Per-step bookkeeping of a lane (t1, SystemOutcome counters, EventMachine
+/// zones): read or written on every step, but not inside the RK stages.
+template <int BLOCK>
+struct Bookkeeping {
+    Real t1[BLOCK];
+    Real smallest[BLOCK];       // SystemOutcome::smallest_step
+    unsigned n_acc[BLOCK], n_rej[BLOCK];
+    int zones[BLOCK];           // zone_of(prev_value[i]), 2 bits per event
+    int steps_in_zone[BLOCK];   // EventMachine::steps_in_zone_
+};
+
 /// Whether a model overrides a HookDefaults no-op (inherited hooks keep the
 /// HookDefaults member-pointer type): per-step hooks that do nothing cost
 /// nothing, not even the shared-memory traffic around them.
@@ -374,7 +385,10 @@ inline constexpr bool kHasOrdinaryAccessory = !std::is_same_v<decltype(&H::ordin
 ///                      when the RHS is large: I-cache, registers);
 ///  * kColdInShared   — cold lane state in shared memory instead of registers;
 ///  * kParamsInShared — per-system parameters in shared memory (one row of
-///                      odd stride per thread, conflict-free 8-byte loads).
+///                      odd stride per thread, conflict-free 8-byte loads);
+///  * kBookInShared   — the per-step bookkeeping (Bookkeeping) in shared
+///                      memory: a few LDS/STS per step for fewer registers
+///                      across the stages (large RHS, high register demand).
 /// ODEGPU_POLICY_{ROLLED,COLD_SHARED,PARAMS_SHARED} override every model in
 /// tuning builds (scripts/build_variants.sh).
 template <class H>
@@ -382,6 +396,7 @@ struct KernelPolicy {
     static constexpr bool kRolledStages = false;
     static constexpr bool kColdInShared = true;
     static constexpr bool kParamsInShared = false;
+    static constexpr bool kBookInShared = false;
 };
 
 template <class H>
@@ -400,6 +415,14 @@ struct EffectivePolicy {
     static constexpr bool kParamsInShared = ODEGPU_POLICY_PARAMS_SHARED && H::kParamCount > 0;
 #else
     static constexpr bool kParamsInShared = KernelPolicy<H>::kParamsInShared && H::kParamCount > 0;
+#endif
+#ifdef ODEGPU_POLICY_BOOK_SHARED
+    static constexpr bool kBookInShared = ODEGPU_POLICY_BOOK_SHARED;
+#else
+    static constexpr bool kBookInShared = [] {
+        if constexpr (requires { KernelPolicy<H>::kBookInShared; }) return KernelPolicy<H>::kBookInShared;
+        else return false; // specialisations written before the flag existed
+    }();
 #endif
     static constexpr int kParamStride = kParamsInShared ? (H::kParamCount | 1) : 1;
     static constexpr int kParamRegs = kParamsInShared ? 1 : (H::kParamCount > 0 ? H::kParamCount : 1);
@@ -425,7 +448,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
     constexpr bool kAdaptive = ALG == Algorithm::RKCK45;
     using Pol = EffectivePolicy<H>;
     static_assert(N <= kMaxDim && E <= kMaxEvents, "model wider than the device controls");
-    constexpr bool kFence = Pol::kColdInShared || Pol::kParamsInShared;
+    constexpr bool kFence = Pol::kColdInShared || Pol::kParamsInShared || Pol::kBookInShared;
 
     // cold state: a shared-memory column per thread, or a register record
     __shared__ ColdState<H, Pol::kColdInShared ? BLOCK : 1> cs_shared;
@@ -445,15 +468,22 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
 #define ODEGPU_C(field) cs.field[tid]
 
     // ---- hot registers: the driver's loop variables (driver.hpp:96-107)
-    Real t = 0, t1 = 0, h = 0, h_step = 0;
-    Real smallest = 0;               // SystemOutcome::smallest_step
+    Real t = 0, h = 0, h_step = 0;
     Real y[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) y[i] = 0;
-    unsigned n_acc = 0, n_rej = 0;   // accepted / rejected steps
-    int zones = 0;                   // zone_of(prev_value[i]), 2 bits per event
-    int steps_in_zone = 0;           // EventMachine::steps_in_zone_
     bool clipped = false;
+    // per-step bookkeeping (t1, smallest step, counters, event zones):
+    // registers, or a shared-memory column when the policy parks it there
+    // to free registers for the stages
+    __shared__ Bookkeeping<Pol::kBookInShared ? BLOCK : 1> bk_shared;
+    Bookkeeping<1> bk_regs;
+    auto& bk = [&]() -> auto& {
+        if constexpr (Pol::kBookInShared) return bk_shared;
+        else return bk_regs;
+    }();
+    const int btid = Pol::kBookInShared ? static_cast<int>(threadIdx.x) : 0;
+#define ODEGPU_B(field) bk.field[btid]
     int phase = kFetch;
 
     const auto load_acc = [&](Real (&a)[A]) {
@@ -467,18 +497,18 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
     // driver.hpp:109-119: clip the next trial step onto t1; false when the
     // system is done (the lane goes to kFinish).
     const auto setup_step = [&]() {
-        if (!(t < t1)) {
+        if (!(t < ODEGPU_B(t1))) {
             phase = kFinish;
             return;
         }
         Real h_try = h;
         clipped = false;
-        if (t + h_try >= t1) {
-            h_try = t1 - t;
+        if (t + h_try >= ODEGPU_B(t1)) {
+            h_try = ODEGPU_B(t1) - t;
             clipped = true;
         }
         if (!(h_try > 0)) { // fp underflow of the remaining span
-            t = t1;
+            t = ODEGPU_B(t1);
             phase = kFinish;
             return;
         }
@@ -493,17 +523,17 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
             const int z = zone_of(fp[i], c.tolerance[i]);
             if (z == kZoneNone) continue; // non-finite: keep the previous arming
             ODEGPU_C(prev_value[i]) = fp[i];
-            zones = with_zone(zones, i, z);
+            ODEGPU_B(zones) = with_zone(ODEGPU_B(zones), i, z);
             any_inside = any_inside || z == kZoneInside;
         }
-        steps_in_zone = any_inside ? steps_in_zone + 1 : 0;
+        ODEGPU_B(steps_in_zone) = any_inside ? ODEGPU_B(steps_in_zone) + 1 : 0;
     };
     // Ends a secant location (driver.hpp:157-164).
     const auto end_secant = [&]() {
         if (!ODEGPU_C(s_conv)) ++ODEGPU_C(n_secf);
         const bool rel = ODEGPU_C(b_th) < ODEGPU_C(h_try);
         ODEGPU_C(relocated) = rel;
-        const Real tl = (ODEGPU_C(clipped) && !rel) ? t1 : t + ODEGPU_C(b_th);
+        const Real tl = (ODEGPU_C(clipped) && !rel) ? ODEGPU_B(t1) : t + ODEGPU_C(b_th);
         ODEGPU_C(t_land) = tl;
         Real yl[N], f[EE];
 #pragma unroll
@@ -533,9 +563,9 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 Real acc[A];
 #pragma unroll
                 for (int i = 0; i < NA; ++i) acc[i] = b.acc[sys + i * n];
-                n_acc = n_rej = 0u;
+                ODEGPU_B(n_acc) = ODEGPU_B(n_rej) = 0u;
                 ODEGPU_C(n_det) = ODEGPU_C(n_secf) = 0u;
-                smallest = __longlong_as_double(0x7ff0000000000000LL); // +inf
+                ODEGPU_B(smallest) = __longlong_as_double(0x7ff0000000000000LL); // +inf
                 ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::ReachedEndTime);
                 // driver.hpp:96-107
                 m.initialize(td[0], S(td, 2), S(y, N), CS(prow, NP), S(acc, NA));
@@ -543,18 +573,18 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 ODEGPU_C(td[1]) = td[1];
                 store_acc(acc);
                 t = td[0];
-                t1 = td[1];
+                ODEGPU_B(t1) = td[1];
                 if constexpr (E > 0) { // EventMachine::init (events.hpp:93-101)
                     Real f0[EE];
                     m.event_values(t, CS(y, N), CS(prow, NP), S(f0, E));
-                    zones = 0;
+                    ODEGPU_B(zones) = 0;
 #pragma unroll
                     for (int i = 0; i < E; ++i) {
                         ODEGPU_C(prev_value[i]) = f0[i];
-                        zones = with_zone(zones, i, zone_of(f0[i], c.tolerance[i]));
+                        ODEGPU_B(zones) = with_zone(ODEGPU_B(zones), i, zone_of(f0[i], c.tolerance[i]));
                         ODEGPU_C(counter[i]) = 0;
                     }
-                    steps_in_zone = 0;
+                    ODEGPU_B(steps_in_zone) = 0;
                 }
                 h = kAdaptive ? sclamp(c.initial_time_step, c.min_step, c.max_step) : c.initial_time_step;
                 phase = kSetup;
@@ -575,8 +605,8 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
 #pragma unroll
                 for (int i = 0; i < N; ++i) y[i] = ODEGPU_C(y_land[i]);
                 t = tl;
-                ++n_acc;
-                smallest = smin(smallest, advanced);
+                ++ODEGPU_B(n_acc);
+                ODEGPU_B(smallest) = smin(ODEGPU_B(smallest), advanced);
                 bool event_stop = false;
                 Real acc[A];
                 load_acc(acc);
@@ -586,7 +616,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     int cnt[EE];
 #pragma unroll
                     for (int i = 0; i < E; ++i) { // EventMachine::commit, events.hpp:134-156
-                        const int kind = classify(zone_at(zones, i), zone_of(ODEGPU_C(f_land[i]), c.tolerance[i]),
+                        const int kind = classify(zone_at(ODEGPU_B(zones), i), zone_of(ODEGPU_C(f_land[i]), c.tolerance[i]),
                                                   c.direction[i]);
                         det[i] = kind != kKindNone || i == located;
                         cnt[i] = ODEGPU_C(counter[i]) + (det[i] ? 1 : 0);
@@ -616,7 +646,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 if (event_stop) {
                     ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::EventStop);
                     phase = kFinish;
-                } else if (E > 0 && steps_in_zone >= c.max_steps_in_zone) {
+                } else if (E > 0 && ODEGPU_B(steps_in_zone) >= c.max_steps_in_zone) {
                     ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::EquilibriumStop);
                     phase = kFinish;
                 } else {
@@ -640,11 +670,11 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 for (int i = 0; i < NA; ++i) b.acc[sys + i * n] = acc[i];
                 b.final_t[sys] = t;
                 b.reason[sys] = ODEGPU_C(reason);
-                b.accepted[sys] = n_acc;
-                b.rejected[sys] = n_rej;
+                b.accepted[sys] = ODEGPU_B(n_acc);
+                b.rejected[sys] = ODEGPU_B(n_rej);
                 b.detections[sys] = ODEGPU_C(n_det);
                 b.secant_failures[sys] = ODEGPU_C(n_secf);
-                b.smallest_step[sys] = smallest;
+                b.smallest_step[sys] = ODEGPU_B(smallest);
                 phase = kFetch;
                 continue;
             }
@@ -724,14 +754,14 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     }
                 }
                 if (!accepted) { // driver.hpp:136-140; t < t1 still holds
-                    ++n_rej;
+                    ++ODEGPU_B(n_rej);
                     h = h_next;
                     setup_step();
                     continue;
                 }
             }
             // accepted: driver.hpp:146-168
-            const Real tl = clipped ? t1 : t + h_try;
+            const Real tl = clipped ? ODEGPU_B(t1) : t + h_try;
             if constexpr (E > 0) {
                 Real f[EE];
                 m.event_values(tl, CS(yn, N), CS(prow, NP), S(f, E));
@@ -740,7 +770,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
 #pragma unroll
                 for (int i = E - 1; i >= 0; --i) {
                     if (located >= 0) break;
-                    const int k = classify(zone_at(zones, i), zone_of(f[i], c.tolerance[i]), c.direction[i]);
+                    const int k = classify(zone_at(ODEGPU_B(zones), i), zone_of(f[i], c.tolerance[i]), c.direction[i]);
                     if (k != kKindNone) {
                         located = i;
                         kind = k;
@@ -794,18 +824,18 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     continue;
                 }
             }
-            smallest = smin(smallest, tl - t);
+            ODEGPU_B(smallest) = smin(ODEGPU_B(smallest), tl - t);
 #pragma unroll
             for (int i = 0; i < N; ++i) y[i] = yn[i];
             t = tl;
-            ++n_acc;
+            ++ODEGPU_B(n_acc);
             if constexpr (kHasOrdinaryAccessory<H>) {
                 Real acc[A];
                 load_acc(acc);
                 m.ordinary_accessory(t, CS(y, N), CS(prow, NP), S(acc, NA));
                 store_acc(acc);
             }
-            if (E > 0 && steps_in_zone >= c.max_steps_in_zone) {
+            if (E > 0 && ODEGPU_B(steps_in_zone) >= c.max_steps_in_zone) {
                 ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::EquilibriumStop);
                 phase = kFinish;
                 continue;
@@ -850,6 +880,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
         }
     }
 #undef ODEGPU_C
+#undef ODEGPU_B
 }
 
 /// The solve kernel. `skip` is the result of the t1 < t0 check queued

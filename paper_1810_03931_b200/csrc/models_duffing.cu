@@ -24,15 +24,15 @@ struct LaunchPolicy<models::DuffingMaxMinHooks> {
 };
 template <>
 struct LaunchPolicy<models::DuffingMaxEventHooks> {
-    static constexpr int kMinBlocks = ODEGPU_MB(7);
+    static constexpr int kMinBlocks = ODEGPU_MB(6);
 };
 template <>
 struct LaunchPolicy<models::DuffingMaxAccessoryHooks> {
-    static constexpr int kMinBlocks = ODEGPU_MB(7);
+    static constexpr int kMinBlocks = ODEGPU_MB(6);
 };
 template <>
 struct LaunchPolicy<models::DuffingHooks> {
-    static constexpr int kMinBlocks = ODEGPU_MB(7);
+    static constexpr int kMinBlocks = ODEGPU_MB(6);
 };
 // 4-dim Lyapunov system: 3 blocks/SM (<= 168 regs) keeps it spill-free.
 template <>

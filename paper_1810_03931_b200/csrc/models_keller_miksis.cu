@@ -6,14 +6,14 @@
 namespace odegpu::device {
 template <>
 struct KernelPolicy<odegpu::models::BubbleCollapseHooks> {
-    static constexpr bool kRolledStages = true, kColdInShared = true, kParamsInShared = true;
+    static constexpr bool kRolledStages = true, kColdInShared = true, kParamsInShared = true, kBookInShared = true;
 };
 } // namespace odegpu::device
 
 namespace odegpu::device {
 template <>
 struct KernelPolicy<odegpu::models::KellerMiksisHooks> {
-    static constexpr bool kRolledStages = true, kColdInShared = true, kParamsInShared = true;
+    static constexpr bool kRolledStages = true, kColdInShared = true, kParamsInShared = true, kBookInShared = true;
 };
 } // namespace odegpu::device
 
@@ -26,11 +26,11 @@ namespace odegpu::detail {
 // stage vectors must stay in registers.
 template <>
 struct LaunchPolicy<models::BubbleCollapseHooks> {
-    static constexpr int kMinBlocks = ODEGPU_MB(4);
+    static constexpr int kMinBlocks = ODEGPU_MB(3);
 };
 template <>
 struct LaunchPolicy<models::KellerMiksisHooks> {
-    static constexpr int kMinBlocks = ODEGPU_MB(4);
+    static constexpr int kMinBlocks = ODEGPU_MB(3);
 };
 
 bool family_dims_keller_miksis(const odegpu_model& m, odegpu_system_dims* d) {

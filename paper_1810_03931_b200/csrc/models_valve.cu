@@ -3,6 +3,15 @@
 #include "launch.cuh"
 #include "odegpu/models/valve.hpp"
 
+namespace odegpu::device {
+// per-step bookkeeping parked in shared memory: 80 registers at 6 blocks/SM
+// without spills (it spills 24 B with the bookkeeping in registers)
+template <>
+struct KernelPolicy<odegpu::models::ValveHooks> {
+    static constexpr bool kRolledStages = false, kColdInShared = true, kParamsInShared = false, kBookInShared = true;
+};
+} // namespace odegpu::device
+
 namespace odegpu::detail {
 
 // Valve: small RHS, straight-line stages, cold state in shared memory,
