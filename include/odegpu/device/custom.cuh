@@ -53,21 +53,25 @@ void solve_custom(SolverBatch& batch, const D& def, const SolverConfig& cfg) {
                                 v.reason, v.accepted_steps, v.rejected_steps, v.event_detections,
                                 v.secant_failures, v.smallest_step, v.capacity, v.count, v.work};
     const H& hooks = def;
-    auto launch = [&](auto kern) {
+    auto launch = [&](auto kern, std::size_t smem) {
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         int resident = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, LP::kBlock, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, LP::kBlock, smem);
         const Index persistent = Index(v.num_sms) * std::max(resident, 1);
         const Index needed = (v.count + LP::kBlock - 1) / LP::kBlock;
         const int grid = static_cast<int>(std::max<Index>(1, std::min(needed, persistent)));
-        kern<<<grid, LP::kBlock, 0, static_cast<cudaStream_t>(v.stream)>>>(hooks, a, ctl, v.skip);
+        kern<<<grid, LP::kBlock, smem, static_cast<cudaStream_t>(v.stream)>>>(hooks, a, ctl, v.skip);
     };
     int prev = -1;
     cudaGetDevice(&prev);
     if (prev != v.device) cudaSetDevice(v.device);
     if (cfg.algorithm == Algorithm::RK4)
-        launch(device::guarded_solve_kernel<H, Algorithm::RK4, LP::kBlock, LP::kMinBlocks>);
+        launch(device::guarded_solve_kernel<H, Algorithm::RK4, LP::kBlock, LP::kMinBlocks>,
+               device::solve_smem_bytes<H, Algorithm::RK4, LP::kBlock>());
     else
-        launch(device::guarded_solve_kernel<H, Algorithm::RKCK45, LP::kBlock, LP::kMinBlocks>);
+        launch(device::guarded_solve_kernel<H, Algorithm::RKCK45, LP::kBlock, LP::kMinBlocks>,
+               device::solve_smem_bytes<H, Algorithm::RKCK45, LP::kBlock>());
     if (prev >= 0 && prev != v.device) cudaSetDevice(prev);
     const int rc = odegpu_custom_end(batch.handle());
     batch.invalidate_host(detail::kSolveWrites);

@@ -19,6 +19,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 #include <span>
 #include <type_traits>
@@ -113,24 +114,28 @@ __device__ __forceinline__ void rhs(const H& m, Real t, const Real (&y)[H::kSyst
 
 /// One trial step from (t, y) with step h (steppers.hpp:82-139). Writes the
 /// proposed state, the embedded error |y5 - y4| (RKCK45) and whether
-/// anything is non-finite.
-/// The stages are a rolled loop around ONE inlined RHS call site: a uniform
-/// switch on the stage index forms the stage argument from the tableau row
-/// and stores the stage derivative, so the (large) RHS — libdevice pow /
-/// sincos for Keller-Miksis — is emitted once instead of 4-6 times and the
-/// step loop fits the instruction cache. Every lane of a warp runs the same
-/// stage, so the switch never diverges. Expressions are those of the
-/// reference, operation for operation.
-template <class H, Algorithm ALG, bool ROLLED, bool FENCE>
+/// anything is non-finite. Expressions are those of the reference, operation
+/// for operation.
+///
+/// ROLLED: the stages are a rolled loop around ONE inlined RHS call site; a
+/// uniform switch on the stage index forms the stage argument from the
+/// tableau row, so a large RHS (libdevice pow / sincos for Keller-Miksis) is
+/// emitted once instead of 4-6 times and the step loop fits the instruction
+/// cache. Every lane of a warp runs the same stage, so the switch never
+/// diverges. The stage derivatives of the rolled loop live in shared memory
+/// (kb: this thread's column, stride BLOCK — conflict-free): a loop-carried
+/// k1..k5 in registers costs ~20 registers across the RHS plus register
+/// moves at every stage, while the smem form costs ~40 LDS/STS per step.
+template <class H, Algorithm ALG, bool ROLLED, int BLOCK>
 __device__ __forceinline__ bool rk_step(const H& m, Real t, Real h, const Real (&y)[H::kSystemDim],
                                         const Real* p, Real (&out)[H::kSystemDim],
-                                        Real (&err)[H::kSystemDim]) {
+                                        Real (&err)[H::kSystemDim], Real* kb) {
     constexpr int N = H::kSystemDim;
-    Real k1[N], k2[N], k3[N], k4[N], k5[N], k6[N];
     bool finite = true;
     if constexpr (!ROLLED) {
         // Straight-line stages: best when the RHS is small (Duffing, valve):
         // no stage dispatch, the scheduler sees across stage boundaries.
+        Real k1[N], k2[N], k3[N], k4[N], k5[N], k6[N];
         Real yt[N];
         if constexpr (ALG == Algorithm::RK4) {
             rhs(m, t, y, p, k1);
@@ -179,107 +184,109 @@ __device__ __forceinline__ bool rk_step(const H& m, Real t, Real h, const Real (
         }
         return !finite;
     }
+    // rolled: k_s (s = 1..STAGES-1) in shared memory, the last one in registers
+#define ODEGPU_K(s, i) kb[((s) - 1) * N * BLOCK + (i) * BLOCK]
+    Real kk[N];
     if constexpr (ALG == Algorithm::RK4) {
 #pragma unroll 1
-        for (int s = 0; s < 4; ++s) {
-            if constexpr (FENCE) cold_fence();
-            Real ts, yt[N], kk[N];
+        for (int s = 1; s <= 4; ++s) {
+            cold_fence();
+            Real ts, yt[N];
             switch (s) {
-            case 0:
+            case 1:
                 ts = t;
 #pragma unroll
                 for (int i = 0; i < N; ++i) yt[i] = y[i];
                 break;
-            case 1:
-                ts = t + 0.5 * h;
-#pragma unroll
-                for (int i = 0; i < N; ++i) yt[i] = y[i] + 0.5 * h * k1[i];
-                break;
             case 2:
                 ts = t + 0.5 * h;
 #pragma unroll
-                for (int i = 0; i < N; ++i) yt[i] = y[i] + 0.5 * h * k2[i];
+                for (int i = 0; i < N; ++i) yt[i] = y[i] + 0.5 * h * ODEGPU_K(1, i);
+                break;
+            case 3:
+                ts = t + 0.5 * h;
+#pragma unroll
+                for (int i = 0; i < N; ++i) yt[i] = y[i] + 0.5 * h * ODEGPU_K(2, i);
                 break;
             default:
                 ts = t + h;
 #pragma unroll
-                for (int i = 0; i < N; ++i) yt[i] = y[i] + h * k3[i];
+                for (int i = 0; i < N; ++i) yt[i] = y[i] + h * ODEGPU_K(3, i);
                 break;
             }
             rhs(m, ts, yt, p, kk);
+            if (s < 4) {
 #pragma unroll
-            for (int i = 0; i < N; ++i) {
-                if (s == 0) k1[i] = kk[i];
-                else if (s == 1) k2[i] = kk[i];
-                else if (s == 2) k3[i] = kk[i];
-                else k4[i] = kk[i];
+                for (int i = 0; i < N; ++i) ODEGPU_K(s, i) = kk[i];
             }
         }
+        cold_fence();
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-            out[i] = y[i] + (h / 6.0) * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
+            out[i] = y[i] + (h / 6.0) * (ODEGPU_K(1, i) + 2.0 * ODEGPU_K(2, i) + 2.0 * ODEGPU_K(3, i) + kk[i]);
             err[i] = 0.0;
             finite = finite && isfinite(out[i]);
         }
     } else {
 #pragma unroll 1
-        for (int s = 0; s < 6; ++s) {
-            if constexpr (FENCE) cold_fence();
-            Real ts, yt[N], kk[N];
+        for (int s = 1; s <= 6; ++s) {
+            cold_fence();
+            Real ts, yt[N];
             switch (s) {
-            case 0:
+            case 1:
                 ts = t;
 #pragma unroll
                 for (int i = 0; i < N; ++i) yt[i] = y[i];
                 break;
-            case 1:
+            case 2:
                 ts = t + ck::c2 * h;
 #pragma unroll
-                for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a21 * k1[i]);
-                break;
-            case 2:
-                ts = t + ck::c3 * h;
-#pragma unroll
-                for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a31 * k1[i] + ck::a32 * k2[i]);
+                for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a21 * ODEGPU_K(1, i));
                 break;
             case 3:
+                ts = t + ck::c3 * h;
+#pragma unroll
+                for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a31 * ODEGPU_K(1, i) + ck::a32 * ODEGPU_K(2, i));
+                break;
+            case 4:
                 ts = t + ck::c4 * h;
 #pragma unroll
                 for (int i = 0; i < N; ++i)
-                    yt[i] = y[i] + h * (ck::a41 * k1[i] + ck::a42 * k2[i] + ck::a43 * k3[i]);
+                    yt[i] = y[i] + h * (ck::a41 * ODEGPU_K(1, i) + ck::a42 * ODEGPU_K(2, i) + ck::a43 * ODEGPU_K(3, i));
                 break;
-            case 4:
+            case 5:
                 ts = t + ck::c5 * h;
 #pragma unroll
                 for (int i = 0; i < N; ++i)
-                    yt[i] = y[i] + h * (ck::a51 * k1[i] + ck::a52 * k2[i] + ck::a53 * k3[i] + ck::a54 * k4[i]);
+                    yt[i] = y[i] + h * (ck::a51 * ODEGPU_K(1, i) + ck::a52 * ODEGPU_K(2, i) +
+                                        ck::a53 * ODEGPU_K(3, i) + ck::a54 * ODEGPU_K(4, i));
                 break;
             default:
                 ts = t + ck::c6 * h;
 #pragma unroll
                 for (int i = 0; i < N; ++i)
-                    yt[i] = y[i] + h * (ck::a61 * k1[i] + ck::a62 * k2[i] + ck::a63 * k3[i] + ck::a64 * k4[i] +
-                                        ck::a65 * k5[i]);
+                    yt[i] = y[i] + h * (ck::a61 * ODEGPU_K(1, i) + ck::a62 * ODEGPU_K(2, i) +
+                                        ck::a63 * ODEGPU_K(3, i) + ck::a64 * ODEGPU_K(4, i) +
+                                        ck::a65 * ODEGPU_K(5, i));
                 break;
             }
             rhs(m, ts, yt, p, kk);
+            if (s < 6) {
 #pragma unroll
-            for (int i = 0; i < N; ++i) {
-                if (s == 0) k1[i] = kk[i];
-                else if (s == 1) k2[i] = kk[i];
-                else if (s == 2) k3[i] = kk[i];
-                else if (s == 3) k4[i] = kk[i];
-                else if (s == 4) k5[i] = kk[i];
-                else k6[i] = kk[i];
+                for (int i = 0; i < N; ++i) ODEGPU_K(s, i) = kk[i];
             }
         }
+        cold_fence();
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-            out[i] = y[i] + h * (ck::b1 * k1[i] + ck::b3 * k3[i] + ck::b4 * k4[i] + ck::b6 * k6[i]);
-            err[i] = fabs(h * (ck::d1 * k1[i] + ck::d3 * k3[i] + ck::d4 * k4[i] + ck::d5 * k5[i] + ck::d6 * k6[i]));
+            out[i] = y[i] + h * (ck::b1 * ODEGPU_K(1, i) + ck::b3 * ODEGPU_K(3, i) + ck::b4 * ODEGPU_K(4, i) +
+                                 ck::b6 * kk[i]);
+            err[i] = fabs(h * (ck::d1 * ODEGPU_K(1, i) + ck::d3 * ODEGPU_K(3, i) + ck::d4 * ODEGPU_K(4, i) +
+                               ck::d5 * ODEGPU_K(5, i) + ck::d6 * kk[i]));
             finite = finite && isfinite(out[i]) && isfinite(err[i]);
         }
     }
+#undef ODEGPU_K
     return !finite;
 }
 
@@ -428,6 +435,23 @@ struct EffectivePolicy {
     static constexpr int kParamRegs = kParamsInShared ? 1 : (H::kParamCount > 0 ? H::kParamCount : 1);
 };
 
+/// Everything a block keeps in shared memory, per policy (dynamic shared
+/// memory: the Keller-Miksis layout exceeds the 48 KB static limit).
+template <class H, Algorithm ALG, int BLOCK>
+struct SharedLayout {
+    using Pol = EffectivePolicy<H>;
+    ColdState<H, Pol::kColdInShared ? BLOCK : 1> cold;
+    Bookkeeping<Pol::kBookInShared ? BLOCK : 1> book;
+    Real params[Pol::kParamsInShared ? BLOCK * Pol::kParamStride : 1];
+    Real k[Pol::kRolledStages ? (ALG == Algorithm::RK4 ? 3 : 5) * H::kSystemDim * BLOCK : 1];
+};
+
+/// Dynamic shared memory of one solve block.
+template <class H, Algorithm ALG, int BLOCK>
+constexpr std::size_t solve_smem_bytes() {
+    return sizeof(SharedLayout<H, ALG, BLOCK>);
+}
+
 /// The ensemble loop. One instantiation per (model, algorithm): hooks are
 /// inlined, widths are compile-time.
 ///
@@ -451,14 +475,18 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
     constexpr bool kFence = Pol::kColdInShared || Pol::kParamsInShared || Pol::kBookInShared;
 
     // cold state: a shared-memory column per thread, or a register record
-    __shared__ ColdState<H, Pol::kColdInShared ? BLOCK : 1> cs_shared;
+    extern __shared__ __align__(16) unsigned char odegpu_dsmem[];
+    auto& sh = *reinterpret_cast<SharedLayout<H, ALG, BLOCK>*>(odegpu_dsmem);
+    auto& cs_shared = sh.cold;
     ColdState<H, 1> cs_regs;
     auto& cs = [&]() -> auto& {
         if constexpr (Pol::kColdInShared) return cs_shared;
         else return cs_regs;
     }();
     const int tid = Pol::kColdInShared ? static_cast<int>(threadIdx.x) : 0;
-    __shared__ Real sp[Pol::kParamsInShared ? BLOCK * Pol::kParamStride : 1];
+    Real* const sp = sh.params;
+    // stage derivatives of the rolled stage loop (rk_step)
+    Real* const kbuf = sh.k + (Pol::kRolledStages ? threadIdx.x : 0);
     const Index n = b.n;
     Real preg[Pol::kParamRegs];
     Real* const prow = Pol::kParamsInShared ? sp + threadIdx.x * Pol::kParamStride : preg;
@@ -476,7 +504,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
     // per-step bookkeeping (t1, smallest step, counters, event zones):
     // registers, or a shared-memory column when the policy parks it there
     // to free registers for the stages
-    __shared__ Bookkeeping<Pol::kBookInShared ? BLOCK : 1> bk_shared;
+    auto& bk_shared = sh.book;
     Bookkeeping<1> bk_regs;
     auto& bk = [&]() -> auto& {
         if constexpr (Pol::kBookInShared) return bk_shared;
@@ -713,7 +741,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
         // ================= the shared Runge-Kutta evaluation
         if constexpr (kFence) cold_fence();
         Real yn[N], err[N];
-        const bool nonfinite = rk_step<H, ALG, Pol::kRolledStages, Pol::kParamsInShared>(m, t, h_step, y, prow, yn, err);
+        const bool nonfinite = rk_step<H, ALG, Pol::kRolledStages, BLOCK>(m, t, h_step, y, prow, yn, err, kbuf);
         if constexpr (kFence) cold_fence();
 
         // ================= ABSORB

@@ -33,10 +33,13 @@ template <class H, Algorithm ALG>
 void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
     constexpr int kMin = LaunchPolicy<H>::kMinBlocks;
     auto kern = guarded_solve_kernel<H, ALG, kBlock, kMin>;
+    constexpr std::size_t smem = dev::solve_smem_bytes<H, ALG, kBlock>();
+    if constexpr (smem > 48 * 1024) // opt-in above the static limit (per device)
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     static int resident = -1; // per instantiation: resident blocks per SM
     if (resident < 0) {
         int r = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kern, kBlock, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kern, kBlock, smem));
         resident = std::max(r, 1);
     }
     const Index n = b->a.count;
@@ -45,7 +48,7 @@ void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
     const int grid = static_cast<int>(std::max<Index>(1, std::min(needed, persistent)));
     CK(cudaMemsetAsync(b->a.work, 0, sizeof(unsigned long long), b->stream));
     CK(cudaEventRecord(b->ev_start, b->stream));
-    kern<<<grid, kBlock, 0, b->stream>>>(hooks, b->a, c, b->first_bad);
+    kern<<<grid, kBlock, smem, b->stream>>>(hooks, b->a, c, b->first_bad);
     CK(cudaGetLastError());
     CK(cudaEventRecord(b->ev_stop, b->stream));
     b->timed = true;

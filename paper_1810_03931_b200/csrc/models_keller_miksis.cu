@@ -26,11 +26,11 @@ namespace odegpu::detail {
 // stage vectors must stay in registers.
 template <>
 struct LaunchPolicy<models::BubbleCollapseHooks> {
-    static constexpr int kMinBlocks = ODEGPU_MB(3);
+    static constexpr int kMinBlocks = ODEGPU_MB(4);
 };
 template <>
 struct LaunchPolicy<models::KellerMiksisHooks> {
-    static constexpr int kMinBlocks = ODEGPU_MB(3);
+    static constexpr int kMinBlocks = ODEGPU_MB(4);
 };
 
 bool family_dims_keller_miksis(const odegpu_model& m, odegpu_system_dims* d) {
