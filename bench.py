@@ -403,7 +403,8 @@ def main():
             "unit": "G lane-FP64-instr/s",
             "frac": achieved / peak_total,
             "traffic": traffic,
-            "algorithmic": f"{wl.instr_per_step} FP64-pipe instructions per trial step (SURVEY.md §8d) x "
+            "algorithmic": f"{wl.instr_per_step} FP64-pipe instructions per trial step (SURVEY.md §8d count, "
+                           f"controller pow as the 13-instruction fifth root; DESIGN.md §3.1) x "
                            f"device-counted trial steps / solve-kernel time (CUDA events on the batch stream)",
             "peak_source": "DFMA microbenchmark in this run (odegpu_dfma_peak, 8 independent chains/thread); "
                            "MEASURED_PEAKS.json has no FP64 entry",

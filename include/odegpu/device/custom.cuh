@@ -66,6 +66,12 @@ void solve_custom(SolverBatch& batch, const D& def, const SolverConfig& cfg) {
     int prev = -1;
     cudaGetDevice(&prev);
     if (prev != v.device) cudaSetDevice(v.device);
+    if constexpr (device::TrigCertifiable<H>) { // see include/odegpu/trig.hpp
+        auto* flags = const_cast<unsigned long long*>(v.skip);
+        cudaMemsetAsync(flags + 1, 0, sizeof(unsigned long long), static_cast<cudaStream_t>(v.stream));
+        const int g = static_cast<int>(std::max<Index>(1, std::min<Index>((v.count + 255) / 256, Index(v.num_sms) * 8)));
+        device::trig_certificate_kernel<H><<<g, 256, 0, static_cast<cudaStream_t>(v.stream)>>>(a, flags);
+    }
     if (cfg.algorithm == Algorithm::RK4)
         launch(device::guarded_solve_kernel<H, Algorithm::RK4, LP::kBlock, LP::kMinBlocks>,
                device::solve_smem_bytes<H, Algorithm::RK4, LP::kBlock>());

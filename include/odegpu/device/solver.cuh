@@ -19,6 +19,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <concepts>
 #include <cstddef>
 #include <cstdint>
 #include <span>
@@ -27,6 +28,7 @@
 #include "odegpu.h"
 #include "odegpu/device/dmath.cuh"
 #include "odegpu/hooks.hpp"
+#include "odegpu/trig.hpp"
 
 namespace odegpu::device {
 
@@ -437,9 +439,8 @@ struct EffectivePolicy {
 
 /// Everything a block keeps in shared memory, per policy (dynamic shared
 /// memory: the Keller-Miksis layout exceeds the 48 KB static limit).
-template <class H, Algorithm ALG, int BLOCK>
+template <class H, Algorithm ALG, int BLOCK, class Pol = EffectivePolicy<H>>
 struct SharedLayout {
-    using Pol = EffectivePolicy<H>;
     ColdState<H, Pol::kColdInShared ? BLOCK : 1> cold;
     Bookkeeping<Pol::kBookInShared ? BLOCK : 1> book;
     Real params[Pol::kParamsInShared ? BLOCK * Pol::kParamStride : 1];
@@ -464,19 +465,18 @@ constexpr std::size_t solve_smem_bytes() {
 /// the next step's clipping — so a lane is ready for its next evaluation
 /// without another trip through the state machine. Only detections, stops
 /// and system ends go back through PREPARE.
-template <class H, Algorithm ALG, int BLOCK>
+template <class H, Algorithm ALG, int BLOCK, class Pol = EffectivePolicy<H>>
 __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, const Controls& c) {
     constexpr int N = H::kSystemDim;
     constexpr int NP = H::kParamCount, NA = H::kAccessoryCount, E = H::kEventCount;
     constexpr int EE = E > 0 ? E : 1, A = NA > 0 ? NA : 1;
     constexpr bool kAdaptive = ALG == Algorithm::RKCK45;
-    using Pol = EffectivePolicy<H>;
     static_assert(N <= kMaxDim && E <= kMaxEvents, "model wider than the device controls");
     constexpr bool kFence = Pol::kColdInShared || Pol::kParamsInShared || Pol::kBookInShared;
 
     // cold state: a shared-memory column per thread, or a register record
     extern __shared__ __align__(16) unsigned char odegpu_dsmem[];
-    auto& sh = *reinterpret_cast<SharedLayout<H, ALG, BLOCK>*>(odegpu_dsmem);
+    auto& sh = *reinterpret_cast<SharedLayout<H, ALG, BLOCK, Pol>*>(odegpu_dsmem);
     auto& cs_shared = sh.cold;
     ColdState<H, 1> cs_regs;
     auto& cs = [&]() -> auto& {
@@ -911,14 +911,47 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
 #undef ODEGPU_B
 }
 
-/// The solve kernel. `skip` is the result of the t1 < t0 check queued
+/// A model whose hooks have a CertifiedTrig twin (include/odegpu/trig.hpp).
+template <class H>
+concept TrigCertifiable = requires(Real t, const Real* p, Index stride) {
+    typename H::certified_hooks;
+    { H::trig_argument_bound(t, t, p, stride) } -> std::convertible_to<Real>;
+} && std::is_empty_v<typename H::certified_hooks> && H::kSystemDim == H::certified_hooks::kSystemDim &&
+    H::kParamCount == H::certified_hooks::kParamCount && H::kEventCount == H::certified_hooks::kEventCount &&
+    H::kAccessoryCount == H::certified_hooks::kAccessoryCount;
+
+/// Trig certificate of a batch: flags[1] stays 0 only if every system that
+/// will be integrated has all trig arguments below kTrigCertifiedLimit over
+/// its time domain (a non-finite bound fails). Reads td plus the parameters
+/// the bound needs; launched right before the solve kernel.
+template <class H>
+__global__ void trig_certificate_kernel(BatchArrays b, unsigned long long* flags) {
+    for (Index i = blockIdx.x * static_cast<Index>(blockDim.x) + threadIdx.x; i < b.count;
+         i += static_cast<Index>(gridDim.x) * blockDim.x) {
+        if (b.reason[i] == static_cast<std::uint8_t>(StopReason::NonFiniteAbort)) continue; // skipped by solve
+        const Real bound = H::trig_argument_bound(b.td[i], b.td[i + b.n], b.params + i, b.n);
+        if (!(bound < kTrigCertifiedLimit)) flags[1] = 1;
+    }
+}
+
+/// The solve kernel. flags[0] is the result of the t1 < t0 check queued
 /// before it: when a system failed it, nothing is integrated (the reference
-/// throws before solving, solve.hpp:159-161).
+/// throws before solving, solve.hpp:159-161). flags[1] == 0 is the batch's
+/// trig certificate: the model's certified_hooks instantiation (no range
+/// branch in its trig) runs instead of the general one; both share one
+/// shared-memory layout and policy.
 template <class H, Algorithm ALG, int BLOCK, int MIN_BLOCKS>
 __global__ void __launch_bounds__(BLOCK, MIN_BLOCKS)
-    guarded_solve_kernel(H model, BatchArrays b, Controls c, const unsigned long long* skip) {
-    if (*skip != ~0ull) return;
-    solve_lanes<H, ALG, BLOCK>(model, b, c);
+    guarded_solve_kernel(H model, BatchArrays b, Controls c, const unsigned long long* flags) {
+    if (flags[0] != ~0ull) return;
+    if constexpr (TrigCertifiable<H>) {
+        if (flags[1] == 0) {
+            solve_lanes<typename H::certified_hooks, ALG, BLOCK, EffectivePolicy<H>>(typename H::certified_hooks{},
+                                                                                   b, c);
+            return;
+        }
+    }
+    solve_lanes<H, ALG, BLOCK, EffectivePolicy<H>>(model, b, c);
 }
 
 /// Kernel controls from the C-ABI structs (materialised once per solve,

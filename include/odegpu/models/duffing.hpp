@@ -9,55 +9,51 @@
 
 #include "odegpu/hooks.hpp"
 #include "odegpu/system.hpp"
-#if defined(__CUDACC__)
-#include "odegpu/device/dmath.cuh"
-#endif
+#include "odegpu/trig.hpp"
 
 namespace odegpu::models {
 
 /// y1' = y2, y2' = delta*y1 - y1^3 - k*y2 + B*cos(omega*t); p = [k, B, delta, omega]
 /// (duffing.hpp:37-42; same operation order).
+template <class T = Trig>
 ODEGPU_HD ODEGPU_INLINE void duffing_rhs(Real t, std::span<const Real> y, std::span<const Real> p,
                                          std::span<Real> dy) {
     const Real k = p[0], B = p[1], delta = p[2], omega = p[3];
     dy[0] = y[1];
-#if defined(__CUDA_ARCH__)
-    const Real c = device::dmath::cos(omega * t); // == ::cos, bitwise (dmath.cuh)
-#else
-    const Real c = std::cos(omega * t);
-#endif
-    dy[1] = delta * y[0] - y[0] * y[0] * y[0] - k * y[1] + B * c;
+    dy[1] = delta * y[0] - y[0] * y[0] * y[0] - k * y[1] + B * T::cos(omega * t);
 }
 
 /// Duffing + linearised radius/angle (duffing.hpp:47-57).
 ODEGPU_HD ODEGPU_INLINE void duffing_lyapunov_rhs(Real t, std::span<const Real> y, std::span<const Real> p,
                                                   std::span<Real> dy) {
-    duffing_rhs(t, y, p, dy);
+    duffing_rhs<Trig>(t, y, p, dy);
     const Real k = p[0], delta = p[2];
     const Real g1 = delta - 3.0 * y[0] * y[0];
     const Real g2 = -k;
     Real s, c;
-#if defined(__CUDA_ARCH__)
-    device::dmath::sincos_fast(y[3], &s, &c);
-#else
-    s = std::sin(y[3]);
-    c = std::cos(y[3]);
-#endif
+    Trig::sincos(y[3], &s, &c); // state-dependent argument: never certified
     dy[2] = y[2] * ((1.0 + g1) * s * c + g2 * s * s);
     dy[3] = -s * s + (g1 * c + g2 * s) * c;
 }
 
-/// DuffingSystem (duffing.hpp:75-88): plain RHS.
-struct DuffingHooks : HookDefaults {
+/// DuffingSystem (duffing.hpp:75-88): plain RHS. The only trig argument is
+/// omega*t, so |argument| <= |omega| max(|t0|, |t1|) certifies a system.
+template <class T = Trig>
+struct DuffingHooksT : HookDefaults {
     static constexpr Index kSystemDim = 2, kParamCount = 4, kEventCount = 0, kAccessoryCount = 0;
     ODEGPU_HD void ode_rhs(Real t, std::span<const Real> y, std::span<const Real> p, std::span<Real> dy) const {
-        duffing_rhs(t, y, p, dy);
+        duffing_rhs<T>(t, y, p, dy);
+    }
+    ODEGPU_HD static Real trig_argument_bound(Real t0, Real t1, const Real* p, Index stride) {
+        return fabs(p[3 * stride]) * fmax(fabs(t0), fabs(t1));
     }
 };
 
 /// DuffingMaxAccessorySystem (duffing.hpp:92-117): running max of y1 + time.
-struct DuffingMaxAccessoryHooks : DuffingHooks {
+template <class T = Trig>
+struct DuffingMaxAccessoryHooksT : DuffingHooksT<T> {
     static constexpr Index kAccessoryCount = 2;
+    using certified_hooks = DuffingMaxAccessoryHooksT<CertifiedTrig>;
     ODEGPU_HD void initialize(Real t, std::span<Real>, std::span<Real> y, std::span<const Real>,
                               std::span<Real> acc) const {
         acc[0] = y[0];
@@ -74,8 +70,10 @@ struct DuffingMaxAccessoryHooks : DuffingHooks {
 
 /// DuffingMaxEventSystem (duffing.hpp:122-156): F = y2 falling locates the
 /// local maxima of y1; the event accessory keeps the largest and its time.
-struct DuffingMaxEventHooks : DuffingHooks {
+template <class T = Trig>
+struct DuffingMaxEventHooksT : DuffingHooksT<T> {
     static constexpr Index kEventCount = 1, kAccessoryCount = 2;
+    using certified_hooks = DuffingMaxEventHooksT<CertifiedTrig>;
     ODEGPU_HD void event_values(Real, std::span<const Real> y, std::span<const Real>, std::span<Real> f) const {
         f[0] = y[1];
     }
@@ -95,8 +93,10 @@ struct DuffingMaxEventHooks : DuffingHooks {
 
 /// cfg1 harness model: per-period max and min of y1 with
 /// their times, acc = [y1_max, t_max, y1_min, t_min], seeded at t0.
-struct DuffingMaxMinHooks : DuffingHooks {
+template <class T = Trig>
+struct DuffingMaxMinHooksT : DuffingHooksT<T> {
     static constexpr Index kAccessoryCount = 4;
+    using certified_hooks = DuffingMaxMinHooksT<CertifiedTrig>;
     ODEGPU_HD void initialize(Real t, std::span<Real>, std::span<Real> y, std::span<const Real>,
                               std::span<Real> acc) const {
         acc[0] = y[0];
@@ -116,6 +116,14 @@ struct DuffingMaxMinHooks : DuffingHooks {
         }
     }
 };
+
+/// Plain Duffing with the certified path.
+struct DuffingHooks : DuffingHooksT<Trig> {
+    using certified_hooks = DuffingHooksT<CertifiedTrig>;
+};
+using DuffingMaxAccessoryHooks = DuffingMaxAccessoryHooksT<Trig>;
+using DuffingMaxEventHooks = DuffingMaxEventHooksT<Trig>;
+using DuffingMaxMinHooks = DuffingMaxMinHooksT<Trig>;
 
 /// DuffingLyapunovSystem (duffing.hpp:162-180): finalize samples the
 /// linearised radius into acc[0] and resets it to one.

@@ -13,9 +13,7 @@
 
 #include "odegpu/hooks.hpp"
 #include "odegpu/system.hpp"
-#if defined(__CUDACC__)
-#include "odegpu/device/dmath.cuh"
-#endif
+#include "odegpu/trig.hpp"
 
 namespace odegpu::models {
 
@@ -23,6 +21,7 @@ namespace odegpu::models {
 /// operation order. y1 <= 0 yields NaN derivatives for the step control.
 /// On the device sin/cos of the same argument share one range reduction
 /// (sincos), as the reference's g++ build merges them into glibc sincos.
+template <class T = Trig>
 ODEGPU_HD ODEGPU_INLINE void keller_miksis_rhs(Real tau, std::span<const Real> y, std::span<const Real> c,
                                                std::span<Real> dy) {
     const Real y1 = y[0], y2 = y[1];
@@ -35,15 +34,8 @@ ODEGPU_HD ODEGPU_INLINE void keller_miksis_rhs(Real tau, std::span<const Real> y
     const Real arg1 = two_pi * tau;
     const Real arg2 = two_pi * c[11] * tau + c[12];
     Real s1, c1, s2, c2;
-#if defined(__CUDA_ARCH__)
-    device::dmath::sincos_fast(arg1, &s1, &c1);
-    device::dmath::sincos_fast(arg2, &s2, &c2);
-#else
-    s1 = std::sin(arg1);
-    c1 = std::cos(arg1);
-    s2 = std::sin(arg2);
-    c2 = std::cos(arg2);
-#endif
+    T::sincos(arg1, &s1, &c1);
+    T::sincos(arg2, &s2, &c2);
 #if defined(__CUDA_ARCH__)
     const Real pw = device::dmath::pow(1.0 / y1, c[10]);
 #else
@@ -57,19 +49,28 @@ ODEGPU_HD ODEGPU_INLINE void keller_miksis_rhs(Real tau, std::span<const Real> y
     dy[1] = numerator / denominator;
 }
 
-/// KellerMiksisSystem (keller_miksis.hpp:106-119).
-struct KellerMiksisHooks : HookDefaults {
+/// KellerMiksisSystem (keller_miksis.hpp:106-119). Trig arguments 2 pi tau and
+/// 2 pi c11 tau + c12: |argument| <= 2 pi max|tau| max(1, |c11|) + |c12|.
+template <class T = Trig>
+struct KellerMiksisHooksT : HookDefaults {
     static constexpr Index kSystemDim = 2, kParamCount = 13, kEventCount = 0, kAccessoryCount = 0;
+    using certified_hooks = KellerMiksisHooksT<CertifiedTrig>;
     ODEGPU_HD void ode_rhs(Real t, std::span<const Real> y, std::span<const Real> p, std::span<Real> dy) const {
-        keller_miksis_rhs(t, y, p, dy);
+        keller_miksis_rhs<T>(t, y, p, dy);
+    }
+    ODEGPU_HD static Real trig_argument_bound(Real t0, Real t1, const Real* p, Index stride) {
+        constexpr Real two_pi = 2.0 * 3.141592653589793238462643383279502884;
+        return two_pi * fmax(fabs(t0), fabs(t1)) * fmax(1.0, fabs(p[11 * stride])) + fabs(p[12 * stride]);
     }
 };
 
 /// BubbleCollapseSystem (keller_miksis.hpp:126-165): runs from one radius
 /// maximum to the next (F = y2 falling, stop at 1); acc = [tau_max, y1_max,
 /// tau_min, y1_min]; finalize moves t0 to the stop time.
-struct BubbleCollapseHooks : KellerMiksisHooks {
+template <class T = Trig>
+struct BubbleCollapseHooksT : KellerMiksisHooksT<T> {
     static constexpr Index kEventCount = 1, kAccessoryCount = 4;
+    using certified_hooks = BubbleCollapseHooksT<CertifiedTrig>;
     ODEGPU_HD void event_values(Real, std::span<const Real> y, std::span<const Real>, std::span<Real> f) const {
         f[0] = y[1];
     }
@@ -92,6 +93,9 @@ struct BubbleCollapseHooks : KellerMiksisHooks {
         time_domain[0] = t;
     }
 };
+
+using KellerMiksisHooks = KellerMiksisHooksT<Trig>;
+using BubbleCollapseHooks = BubbleCollapseHooksT<Trig>;
 
 // ----------------------------------------------------------- host classes
 

@@ -323,6 +323,12 @@ class SolverBatch:
                     event_detections=d.event_detections, secant_failures=d.secant_failures,
                     reason_counts=list(d.reason_counts), max_trial_steps=d.max_trial_steps)
 
+    def trig_certified(self) -> bool:
+        """Whether the last solve ran the certified (branch-free trig) path."""
+        v = C.c_int()
+        check(self._lib.odegpu_batch_trig_certified(self._h, C.byref(v)))
+        return bool(v.value)
+
     def last_kernel_ms(self) -> float:
         v = C.c_double()
         check(self._lib.odegpu_batch_last_kernel_ms(self._h, C.byref(v)))

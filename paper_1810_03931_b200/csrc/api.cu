@@ -153,7 +153,7 @@ odegpu_batch* batch_create(const odegpu_batch_dims& dims, int device) {
                                 n,                          // reason
                                 n * 8, n * 8, n * 8, n * 8, // counters
                                 n * 8,                      // smallest_step
-                                8, 8, 128};                 // work, first_bad, diag
+                                8, 16, 128};                // work, first_bad + trig flag, diag
         constexpr int kArrays = sizeof(sizes) / sizeof(sizes[0]);
         size_t total = 0;
         for (size_t s : sizes) total += align_up(s);
@@ -518,6 +518,18 @@ int odegpu_batch_diagnostics(odegpu_batch* b, odegpu_diagnostics* out) {
         out->secant_failures = static_cast<Index>(h[3]);
         for (int k = 0; k < 4; ++k) out->reason_counts[k] = static_cast<Index>(h[4 + k]);
         out->max_trial_steps = static_cast<Index>(h[8]);
+    });
+}
+
+int odegpu_batch_trig_certified(odegpu_batch* b, int* certified) {
+    return guarded([&] {
+        check_batch(b);
+        if (!certified) throw_invalid("null argument");
+        DeviceGuard g(b->device);
+        unsigned long long f[2] = {0, 0};
+        CK(cudaMemcpyAsync(f, b->first_bad, sizeof(f), cudaMemcpyDeviceToHost, b->stream));
+        CK(cudaStreamSynchronize(b->stream));
+        *certified = (b->timed && f[1] == 0) ? 1 : 0;
     });
 }
 

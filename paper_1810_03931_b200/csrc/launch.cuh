@@ -46,6 +46,12 @@ void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
     const Index persistent = Index(b->num_sms) * resident;
     const Index needed = (n + kBlock - 1) / kBlock;
     const int grid = static_cast<int>(std::max<Index>(1, std::min(needed, persistent)));
+    if constexpr (dev::TrigCertifiable<H>) {
+        CK(cudaMemsetAsync(b->first_bad + 1, 0, sizeof(unsigned long long), b->stream));
+        dev::trig_certificate_kernel<H><<<grid_for(b, b->a.count, 256), 256, 0, b->stream>>>(b->a, b->first_bad);
+        CK(cudaGetLastError());
+        ++b->launches;
+    }
     CK(cudaMemsetAsync(b->a.work, 0, sizeof(unsigned long long), b->stream));
     CK(cudaEventRecord(b->ev_start, b->stream));
     kern<<<grid, kBlock, smem, b->stream>>>(hooks, b->a, c, b->first_bad);

@@ -100,7 +100,10 @@ class Workload:
     y: np.ndarray  # [n, N]
     p: np.ndarray  # [np, N]
     acc: np.ndarray  # [na, N]
-    instr_per_step: int  # FP64-pipe instructions per trial step
+    # FP64-pipe instructions per trial step: SURVEY.md §8d's count from the
+    # reference formulas, with the controller's pow(ratio, -0.2) (80) costed
+    # as the kernels' 13-instruction Newton fifth root
+    instr_per_step: int
     flops_per_step: int
 
     @property
@@ -151,7 +154,7 @@ def cfg2(nk: int = 1024, nb: int = 1024) -> Workload:
     td = np.stack([np.zeros(n), np.full(n, TWO_PI)])
     model = DuffingMaxEventSystem(1e-6, 0, OdeControls.uniform(2, 1e-9, 1e-9))
     return Workload("cfg2_duffing_rkck45_event", f"Duffing RKCK45 tol 1e-9 + event F=y2, k x B = {nk}x{nb}",
-                    model, abi.RKCK45, 1e-3, 32, td, np.zeros((2, n)), p, np.zeros((2, n)), 289, 485)
+                    model, abi.RKCK45, 1e-3, 32, td, np.zeros((2, n)), p, np.zeros((2, n)), 222, 382)
 
 
 def cfg3(npa: int = 1024, nf: int = 1024, transient: int = 64, saved: int = 8) -> Workload:
@@ -164,7 +167,7 @@ def cfg3(npa: int = 1024, nf: int = 1024, transient: int = 64, saved: int = 8) -
     y = np.stack([np.ones(n), np.zeros(n)])
     model = BubbleCollapseSystem(1e-6, OdeControls.uniform(2, 1e-10, 1e-10))
     return Workload("cfg3_keller_miksis", f"Keller-Miksis RKCK45 tol 1e-10 collapse, PA1 x f1 = {npa}x{nf}",
-                    model, abi.RKCK45, 1e-3, transient + saved, td, y, c, np.zeros((4, n)), 1261, 2075)
+                    model, abi.RKCK45, 1e-3, transient + saved, td, y, c, np.zeros((4, n)), 1194, 1972)
 
 
 def cfg4(n: int = 1 << 19, transient: int = 256, saved: int = 32) -> Workload:
@@ -176,7 +179,7 @@ def cfg4(n: int = 1 << 19, transient: int = 256, saved: int = 32) -> Workload:
     y = np.stack([np.full(n, 0.2), np.zeros(n), np.full(n, delta + 0.2)])
     model = ValveSystem(1e-6, OdeControls.uniform(3, 1e-10, 1e-10))
     return Workload("cfg4_valve", f"Valve RKCK45 tol 1e-10, 2 events + impact action, q sweep N={n}",
-                    model, abi.RKCK45, 1e-3, transient + saved, td, y, p, np.zeros((2, n)), 287, 474)
+                    model, abi.RKCK45, 1e-3, transient + saved, td, y, p, np.zeros((2, n)), 220, 371)
 
 
 def cfg5(log2n: int) -> Workload:
