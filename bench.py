@@ -288,6 +288,7 @@ def main():
             e1.synchronize()
             ev_ms.append(e0.elapsed_time(e1))
             kern_ms.append(batch.last_kernel_ms())
+            certified = batch.trig_certified()
             d = batch.diagnostics()
             steps_total += d["accepted_steps"] + d["rejected_steps"]
             max_trial = max(max_trial, d["max_trial_steps"])
@@ -390,6 +391,7 @@ def main():
             "algorithm": "RK4" if wl.algorithm == abi.RK4 else "RKCK45",
             "l2": "flushed between steps (256 MiB write outside the timed events)",
             "parallelism": f"replicas{world}" if world > 1 else "single GPU",
+            "trig_path": "certified (branch-free, include/odegpu/trig.hpp)" if certified else "general",
         },
         "systems_per_s": sys_total / elapsed,
         "trial_steps_per_system_step": steps_total / max(sys_total, 1),
