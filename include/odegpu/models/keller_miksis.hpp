@@ -37,13 +37,29 @@ ODEGPU_HD ODEGPU_INLINE void keller_miksis_rhs(Real tau, std::span<const Real> y
     T::sincos(arg1, &s1, &c1);
     T::sincos(arg2, &s2, &c2);
 #if defined(__CUDA_ARCH__)
-    const Real pw = device::dmath::pow(1.0 / y1, c[10]);
+    // 1/y1, c3/y1 and c4 y2/y1 share one reciprocal of y1 (bitwise the same
+    // quotients), and pow takes its branch-free form; one rarely taken
+    // branch redoes all four the general way when an operand leaves their
+    // range (dmath.cuh: Divisor, pow_lean).
+    device::dmath::Divisor by_y1(y1);
+    Real inv = by_y1.div(1.0);
+    Real q3 = by_y1.div(c[3]);
+    Real q4 = by_y1.div(c[4] * y2);
+    bool lean = true;
+    Real pw = device::dmath::pow_lean(inv, c[10], &lean);
+    if (!(by_y1.ok() && lean)) {
+        inv = 1.0 / y1;
+        q3 = c[3] / y1;
+        q4 = c[4] * y2 / y1;
+        pw = device::dmath::pow(inv, c[10]);
+    }
 #else
     const Real pw = std::pow(1.0 / y1, c[10]);
+    const Real q3 = c[3] / y1, q4 = c[4] * y2 / y1;
 #endif
-    const Real numerator = (c[0] + c[1] * y2) * pw - c[2] * (1.0 + c[9] * y2) - c[3] / y1 -
-                           c[4] * y2 / y1 - (1.0 - c[9] * y2 / 3.0) * 1.5 * y2 * y2 -
-                           (c[5] * s1 + c[6] * s2) * (1.0 + c[9] * y2) - y1 * (c[7] * c1 + c[8] * c2);
+    const Real numerator = (c[0] + c[1] * y2) * pw - c[2] * (1.0 + c[9] * y2) - q3 - q4 -
+                           (1.0 - c[9] * y2 / 3.0) * 1.5 * y2 * y2 - (c[5] * s1 + c[6] * s2) * (1.0 + c[9] * y2) -
+                           y1 * (c[7] * c1 + c[8] * c2);
     const Real denominator = y1 - c[9] * y1 * y2 + c[4] * c[9];
     dy[0] = y2;
     dy[1] = numerator / denominator;
