@@ -375,6 +375,7 @@ struct ColdState {
 template <int BLOCK>
 struct Bookkeeping {
     Real t1[BLOCK];
+    Real h[BLOCK];              // the driver's step size (driver.hpp:105)
     Real smallest[BLOCK];       // SystemOutcome::smallest_step
     unsigned n_acc[BLOCK], n_rej[BLOCK];
     int zones[BLOCK];           // zone_of(prev_value[i]), 2 bits per event
@@ -496,7 +497,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
 #define ODEGPU_C(field) cs.field[tid]
 
     // ---- hot registers: the driver's loop variables (driver.hpp:96-107)
-    Real t = 0, h = 0, h_step = 0;
+    Real t = 0, h_step = 0;
     Real y[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) y[i] = 0;
@@ -529,7 +530,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
             phase = kFinish;
             return;
         }
-        Real h_try = h;
+        Real h_try = ODEGPU_B(h);
         clipped = false;
         if (t + h_try >= ODEGPU_B(t1)) {
             h_try = ODEGPU_B(t1) - t;
@@ -614,7 +615,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     }
                     ODEGPU_B(steps_in_zone) = 0;
                 }
-                h = kAdaptive ? sclamp(c.initial_time_step, c.min_step, c.max_step) : c.initial_time_step;
+                ODEGPU_B(h) = kAdaptive ? sclamp(c.initial_time_step, c.min_step, c.max_step) : c.initial_time_step;
                 phase = kSetup;
             }
             if (phase == kSetup) {
@@ -678,7 +679,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::EquilibriumStop);
                     phase = kFinish;
                 } else {
-                    if (kAdaptive && !ODEGPU_C(relocated)) h = ODEGPU_C(h_next);
+                    if (kAdaptive && !ODEGPU_C(relocated)) ODEGPU_B(h) = ODEGPU_C(h_next);
                     setup_step();
                 }
                 continue;
@@ -747,7 +748,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
         // ================= ABSORB
         if (phase == kReadyStep) {
             const Real h_try = h_step;
-            Real h_next = h;
+            Real h_next = ODEGPU_B(h);
             if constexpr (!kAdaptive) {
                 if (nonfinite) { // driver.hpp:124-128
                     ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::NonFiniteAbort);
@@ -783,7 +784,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 }
                 if (!accepted) { // driver.hpp:136-140; t < t1 still holds
                     ++ODEGPU_B(n_rej);
-                    h = h_next;
+                    ODEGPU_B(h) = h_next;
                     setup_step();
                     continue;
                 }
@@ -868,7 +869,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 phase = kFinish;
                 continue;
             }
-            h = h_next;
+            ODEGPU_B(h) = h_next;
             setup_step();
         } else if (phase == kReadySecant) { // one secant iteration's step is in (events.hpp:222-240)
             if constexpr (E > 0) {

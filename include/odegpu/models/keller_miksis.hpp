@@ -37,32 +37,45 @@ ODEGPU_HD ODEGPU_INLINE void keller_miksis_rhs(Real tau, std::span<const Real> y
     T::sincos(arg1, &s1, &c1);
     T::sincos(arg2, &s2, &c2);
 #if defined(__CUDA_ARCH__)
-    // 1/y1, c3/y1 and c4 y2/y1 share one reciprocal of y1 (bitwise the same
-    // quotients), and pow takes its branch-free form; one rarely taken
-    // branch redoes all four the general way when an operand leaves their
-    // range (dmath.cuh: Divisor, pow_lean).
+    // Every quotient of the RHS through the division fast path without its
+    // per-division branch (1/y1, c3/y1 and c4 y2/y1 share one reciprocal of
+    // y1; /3 uses RN(1/3)) and pow in its branch-free form — bitwise the
+    // same values (dmath.cuh: Divisor, pow_lean). The RHS is straight-line
+    // code the scheduler can interleave; two rarely taken branches redo the
+    // quotients the general way when an operand leaves the fast forms' range.
     device::dmath::Divisor by_y1(y1);
-    Real inv = by_y1.div(1.0);
+    device::dmath::Divisor by_3(3.0, 1.0 / 3.0);
+    Real inv = by_y1.reciprocal();
     Real q3 = by_y1.div(c[3]);
     Real q4 = by_y1.div(c[4] * y2);
+    Real third = by_3.div(c[9] * y2);
     bool lean = true;
     Real pw = device::dmath::pow_lean(inv, c[10], &lean);
-    if (!(by_y1.ok() && lean)) {
+    if (!(by_y1.ok() && by_3.ok() && lean)) {
         inv = 1.0 / y1;
         q3 = c[3] / y1;
         q4 = c[4] * y2 / y1;
+        third = c[9] * y2 / 3.0;
         pw = device::dmath::pow(inv, c[10]);
     }
+    const Real numerator = (c[0] + c[1] * y2) * pw - c[2] * (1.0 + c[9] * y2) - q3 - q4 -
+                           (1.0 - third) * 1.5 * y2 * y2 - (c[5] * s1 + c[6] * s2) * (1.0 + c[9] * y2) -
+                           y1 * (c[7] * c1 + c[8] * c2);
+    const Real denominator = y1 - c[9] * y1 * y2 + c[4] * c[9];
+    device::dmath::Divisor by_den(denominator);
+    Real ddy = by_den.div(numerator);
+    if (!by_den.ok()) ddy = numerator / denominator;
+    dy[0] = y2;
+    dy[1] = ddy;
 #else
     const Real pw = std::pow(1.0 / y1, c[10]);
-    const Real q3 = c[3] / y1, q4 = c[4] * y2 / y1;
-#endif
-    const Real numerator = (c[0] + c[1] * y2) * pw - c[2] * (1.0 + c[9] * y2) - q3 - q4 -
+    const Real numerator = (c[0] + c[1] * y2) * pw - c[2] * (1.0 + c[9] * y2) - c[3] / y1 - c[4] * y2 / y1 -
                            (1.0 - c[9] * y2 / 3.0) * 1.5 * y2 * y2 - (c[5] * s1 + c[6] * s2) * (1.0 + c[9] * y2) -
                            y1 * (c[7] * c1 + c[8] * c2);
     const Real denominator = y1 - c[9] * y1 * y2 + c[4] * c[9];
     dy[0] = y2;
     dy[1] = numerator / denominator;
+#endif
 }
 
 /// KellerMiksisSystem (keller_miksis.hpp:106-119). Trig arguments 2 pi tau and
