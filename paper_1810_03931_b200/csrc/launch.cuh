@@ -22,6 +22,7 @@ using dev::guarded_solve_kernel;
 
 template <class H>
 struct LaunchPolicy {
+    static constexpr int kBlock = detail::kBlock;
 #ifdef ODEGPU_MIN_BLOCKS
     static constexpr int kMinBlocks = ODEGPU_MIN_BLOCKS;
 #else
@@ -32,6 +33,10 @@ struct LaunchPolicy {
 template <class H, Algorithm ALG>
 void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
     constexpr int kMin = LaunchPolicy<H>::kMinBlocks;
+    constexpr int kBlock = [] {
+        if constexpr (requires { LaunchPolicy<H>::kBlock; }) return LaunchPolicy<H>::kBlock;
+        else return detail::kBlock;
+    }();
     auto kern = guarded_solve_kernel<H, ALG, kBlock, kMin>;
     constexpr std::size_t smem = dev::solve_smem_bytes<H, ALG, kBlock>();
     if constexpr (smem > 48 * 1024) // opt-in above the static limit (per device)

@@ -20,6 +20,9 @@ namespace odegpu::detail {
 //   enough registers (123 -> 72) for 7 blocks of 128 threads per SM.
 template <>
 struct LaunchPolicy<models::DuffingMaxMinHooks> {
+#ifdef ODEGPU_CFG1_BLOCK
+    static constexpr int kBlock = ODEGPU_CFG1_BLOCK;
+#endif
     static constexpr int kMinBlocks = ODEGPU_MB(1);
 };
 template <>
