@@ -756,7 +756,9 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     continue;
                 }
             } else {
-                // error_ratio (steppers.hpp:154-163) + control_step (176-198)
+                // error_ratio (steppers.hpp:154-163) + control_step (176-198).
+                // (The branch-free Divisor form of these quotients measured
+                // slower here: 2.27 vs 2.16 ms on cfg2.)
                 Real ratio = 0.0;
 #pragma unroll
                 for (int i = 0; i < N; ++i) {
