@@ -65,6 +65,17 @@ struct BatchArrays {
     Index n;                  // stride (batch capacity)
     Index count;              // systems [0, count) are integrated (count <= n)
     unsigned long long* work; // next system to hand out (zeroed before launch)
+    // Scan tallies (ScanDiagnostics, scan.hpp:41-49), accumulated across
+    // solves when non-null: [6] detections outside their zone, [7] max
+    // |F|/tolerance over detections (bits of a non-negative double), [8]
+    // systems whose t0 did not advance over the solve (see kTally*).
+    unsigned long long* tally = nullptr;
+};
+
+/// Slots of the scan tally (shared with the tally kernel, csrc/kernels.cu).
+enum : int {
+    kTallyReason0 = 0, kTallySecantFailures = 4, kTallyDetections = 5, kTallyOutsideZone = 6,
+    kTallyMaxRatio = 7, kTallyStartNotAdvanced = 8, kTallyNonfinite = 9, kTallySlots = 10
 };
 
 // --- Cash-Karp tableau (steppers.hpp:16-39): exact rationals rendered once.
@@ -362,6 +373,10 @@ struct ColdState {
     Real f_land[E][BLOCK];
     Real prev_value[E][BLOCK]; // EventMachine (events.hpp:76-178)
     Real h_try[BLOCK], h_next[BLOCK], t_land[BLOCK];
+    Real td0_in[BLOCK];            // td[0] as fetched (scan t0-advance check)
+    Real lane_max_ratio[BLOCK];    // lane accumulators for the scan tally,
+    unsigned lane_outside[BLOCK];  // over every system the lane integrates
+    unsigned lane_not_advanced[BLOCK];
     Real th_prev[BLOCK], f_prev[BLOCK], th_cur[BLOCK], f_cur[BLOCK], th_min[BLOCK], b_th[BLOCK], b_f[BLOCK];
     long long sys[BLOCK];
     unsigned n_det[BLOCK], n_secf[BLOCK];
@@ -478,11 +493,10 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
     // cold state: a shared-memory column per thread, or a register record
     extern __shared__ __align__(16) unsigned char odegpu_dsmem[];
     auto& sh = *reinterpret_cast<SharedLayout<H, ALG, BLOCK, Pol>*>(odegpu_dsmem);
-    auto& cs_shared = sh.cold;
     ColdState<H, 1> cs_regs;
-    auto& cs = [&]() -> auto& {
-        if constexpr (Pol::kColdInShared) return cs_shared;
-        else return cs_regs;
+    auto& cs = *[&] {
+        if constexpr (Pol::kColdInShared) return &sh.cold;
+        else return &cs_regs;
     }();
     const int tid = Pol::kColdInShared ? static_cast<int>(threadIdx.x) : 0;
     Real* const sp = sh.params;
@@ -505,11 +519,10 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
     // per-step bookkeeping (t1, smallest step, counters, event zones):
     // registers, or a shared-memory column when the policy parks it there
     // to free registers for the stages
-    auto& bk_shared = sh.book;
     Bookkeeping<1> bk_regs;
-    auto& bk = [&]() -> auto& {
-        if constexpr (Pol::kBookInShared) return bk_shared;
-        else return bk_regs;
+    auto& bk = *[&] {
+        if constexpr (Pol::kBookInShared) return &sh.book;
+        else return &bk_regs;
     }();
     const int btid = Pol::kBookInShared ? static_cast<int>(threadIdx.x) : 0;
 #define ODEGPU_B(field) bk.field[btid]
@@ -573,6 +586,10 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
         phase = kCommit;
     };
 
+    ODEGPU_C(lane_max_ratio) = 0.0;
+    ODEGPU_C(lane_outside) = 0u;
+    ODEGPU_C(lane_not_advanced) = 0u;
+
     for (;;) {
         // ================= PREPARE: bring this lane to a pending RK evaluation
         while (phase < kDone) {
@@ -585,6 +602,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 if (b.reason[sys] == static_cast<std::uint8_t>(StopReason::NonFiniteAbort)) continue; // solve.hpp:98
                 ODEGPU_C(sys) = sys;
                 Real td[2] = {b.td[sys], b.td[sys + n]};
+                ODEGPU_C(td0_in) = td[0];
 #pragma unroll
                 for (int i = 0; i < N; ++i) y[i] = b.state[sys + i * n];
 #pragma unroll
@@ -650,7 +668,16 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                         det[i] = kind != kKindNone || i == located;
                         cnt[i] = ODEGPU_C(counter[i]) + (det[i] ? 1 : 0);
                         ODEGPU_C(counter[i]) = cnt[i];
-                        if (det[i]) ++ODEGPU_C(n_det);
+                        if (det[i]) {
+                            ++ODEGPU_C(n_det);
+                            // what the scans' detection observer records
+                            // (src/scan.cpp:51-61): |F|/tol and in-zone
+                            const Real v = ODEGPU_C(f_land[i]);
+                            const bool fin = isfinite(v);
+                            const Real ratio = fin ? fabs(v) / c.tolerance[i] : __longlong_as_double(0x7ff0000000000000LL);
+                            if (!(fin && fabs(v) <= c.tolerance[i])) ++ODEGPU_C(lane_outside);
+                            ODEGPU_C(lane_max_ratio) = smax(ODEGPU_C(lane_max_ratio), ratio);
+                        }
                     }
                     Real f_post[EE];
                     if (located >= 0) {
@@ -704,6 +731,9 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 b.detections[sys] = ODEGPU_C(n_det);
                 b.secant_failures[sys] = ODEGPU_C(n_secf);
                 b.smallest_step[sys] = ODEGPU_B(smallest);
+                if (ODEGPU_C(reason) != static_cast<std::uint8_t>(StopReason::NonFiniteAbort) &&
+                    !(td[0] > ODEGPU_C(td0_in)))
+                    ++ODEGPU_C(lane_not_advanced); // scan.cpp:296-298
                 phase = kFetch;
                 continue;
             }
@@ -737,7 +767,23 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
         // is done, and the vote re-converges the warp, so the RK stages below
         // always run once per iteration for all lanes (finished lanes compute
         // on stale state and ignore the result).
-        if (__all_sync(0xffffffffu, phase == kDone)) break;
+        if (__all_sync(0xffffffffu, phase == kDone)) {
+            if (b.tally) { // warp-reduced scan tally, one atomic per counter and warp
+                unsigned outside = ODEGPU_C(lane_outside), not_adv = ODEGPU_C(lane_not_advanced);
+                Real mr = ODEGPU_C(lane_max_ratio);
+                for (int o = 16; o > 0; o >>= 1) {
+                    outside += __shfl_xor_sync(0xffffffffu, outside, o);
+                    not_adv += __shfl_xor_sync(0xffffffffu, not_adv, o);
+                    mr = smax(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+                }
+                if ((threadIdx.x & 31) == 0) {
+                    if (outside) atomicAdd(b.tally + kTallyOutsideZone, static_cast<unsigned long long>(outside));
+                    if (not_adv) atomicAdd(b.tally + kTallyStartNotAdvanced, static_cast<unsigned long long>(not_adv));
+                    if (mr > 0) atomicMax(b.tally + kTallyMaxRatio, static_cast<unsigned long long>(__double_as_longlong(mr)));
+                }
+            }
+            break;
+        }
 
         // ================= the shared Runge-Kutta evaluation
         if constexpr (kFence) cold_fence();

@@ -116,5 +116,26 @@ def solve_workload(which: str, wl, iterations: int | None = None, trace: bool = 
     return dict(td=td, y=y, p=p, acc=acc, outcomes=oc, seconds=secs, trace=tr)
 
 
+def scan(protocol: int, spec, workers: int = 0):
+    """The reference's scan protocol (src/scan.cpp) on the same C spec as
+    odegpu_scan_run: (rows, diagnostics dict)."""
+    from paper_1810_03931_b200 import scan as gscan
+
+    lib = load("reference")
+    f = lib.odref_scan_run
+    f.restype = C.c_int
+    f.argtypes = [C.c_int32, C.c_void_p, C.POINTER(C.c_double), abi.Index, C.POINTER(abi.Index),
+                  C.POINTER(abi.Index), C.POINTER(abi.ScanDiagnosticsC), C.c_int]
+    cols = gscan.COLUMNS[protocol]
+    rows = np.zeros((gscan.expected_rows(protocol, spec), len(cols)))
+    nr, nc, d = abi.Index(), abi.Index(), abi.ScanDiagnosticsC()
+    c_spec = spec.to_c()
+    rc = f(protocol, C.byref(c_spec), rows.ctypes.data_as(C.POINTER(C.c_double)), rows.shape[0], C.byref(nr),
+           C.byref(nc), C.byref(d), workers or host_cores())
+    if rc != 0:
+        raise CheckerError(rc, lib.odref_last_error().decode())
+    return rows[: nr.value], gscan.diagnostics_dict(d)
+
+
 def host_cores() -> int:
     return len(os.sched_getaffinity(0))

@@ -316,4 +316,110 @@ int odref_param_range(double lo, double hi, odegpu_index res, int log_scale, dou
     }
 }
 
+// The reference's scan protocols (src/scan.cpp:145-370) on the same C specs
+// as odegpu_scan_run (include/odegpu.h): rows row-major, diagnostics.
+static scan::ParamRange ref_range(const odegpu_param_range& r) {
+    return scan::ParamRange{r.min, r.max, r.res, r.log_scale ? scan::Scale::Log : scan::Scale::Linear};
+}
+static scan::SolveOptions ref_options(const odegpu_scan_options& o, int workers) {
+    scan::SolveOptions s;
+    s.algorithm = o.algorithm == ODEGPU_RK4 ? Algorithm::RK4 : Algorithm::RKCK45;
+    s.dt = o.dt;
+    s.rel_tol = o.rel_tol;
+    s.abs_tol = o.abs_tol;
+    s.event_tol = o.event_tol;
+    s.batch_capacity = o.batch_capacity;
+    s.workers = workers;
+    return s;
+}
+
+int odref_scan_run(int32_t protocol, const void* spec, double* rows, odegpu_index max_rows, odegpu_index* n_rows,
+                   odegpu_index* n_columns, odegpu_scan_diagnostics* diag, int workers) {
+    try {
+        scan::ScanResult r;
+        if (protocol <= ODEGPU_SCAN_DUFFING_LYAPUNOV) {
+            const auto& d = *static_cast<const odegpu_duffing_scan*>(spec);
+            scan::DuffingScanSpec s;
+            s.k = ref_range(d.k);
+            s.forcing_amplitude = d.forcing_amplitude;
+            s.stiffness = d.stiffness;
+            s.forcing_omega = d.forcing_omega;
+            s.ic = {d.ic[0], d.ic[1]};
+            s.transient = d.transient;
+            s.saved = d.saved;
+            s.solver = ref_options(d.solver, workers);
+            if (protocol == ODEGPU_SCAN_DUFFING_POINCARE) r = scan::run_duffing_poincare(s);
+            else if (protocol == ODEGPU_SCAN_DUFFING_LYAPUNOV) r = scan::run_duffing_lyapunov(s);
+            else
+                r = scan::run_duffing_maxima(s, protocol == ODEGPU_SCAN_DUFFING_MAXIMA_EVENT ? scan::MaximaMode::Event
+                                                                                              : scan::MaximaMode::Accessory);
+        } else if (protocol == ODEGPU_SCAN_BUBBLE) {
+            const auto& b = *static_cast<const odegpu_bubble_scan*>(spec);
+            scan::BubbleScanSpec s;
+            s.pa1_bar = ref_range(b.pa1_bar);
+            s.pa2_bar = ref_range(b.pa2_bar);
+            s.f1_khz = ref_range(b.f1_khz);
+            s.f2_khz = ref_range(b.f2_khz);
+            s.material.R_E = b.R_E;
+            s.material.c_L = b.c_L;
+            s.material.rho_L = b.rho_L;
+            s.material.P_inf = b.P_inf;
+            s.material.p_V = b.p_V;
+            s.material.sigma = b.sigma;
+            s.material.mu_L = b.mu_L;
+            s.material.gamma = b.gamma;
+            s.material.theta = b.theta;
+            s.ic = {b.ic[0], b.ic[1]};
+            s.t_end = b.t_end;
+            s.transient = b.transient;
+            s.saved = b.saved;
+            s.solver = ref_options(b.solver, workers);
+            r = scan::run_bubble_scan(s);
+        } else if (protocol == ODEGPU_SCAN_VALVE) {
+            const auto& v = *static_cast<const odegpu_valve_scan*>(spec);
+            scan::ValveScanSpec s;
+            s.q = ref_range(v.q);
+            s.kappa = v.kappa;
+            s.delta = v.delta;
+            s.beta = v.beta;
+            s.restitution = v.restitution;
+            s.ic = {v.ic[0], v.ic[1], v.ic[2]};
+            s.t_end = v.t_end;
+            s.transient = v.transient;
+            s.saved = v.saved;
+            s.solver = ref_options(v.solver, workers);
+            r = scan::run_valve_scan(s);
+        } else {
+            g_err = "scan: unknown protocol";
+            return ODEGPU_ERR_INVALID_ARGUMENT;
+        }
+        const odegpu_index nr = std::ssize(r.rows), nc = std::ssize(r.columns);
+        *n_rows = nr;
+        *n_columns = nc;
+        if (rows) {
+            if (max_rows < nr) {
+                g_err = "scan: rows buffer too small";
+                return ODEGPU_ERR_OUT_OF_RANGE;
+            }
+            for (odegpu_index i = 0; i < nr; ++i)
+                std::memcpy(rows + i * nc, r.rows[static_cast<std::size_t>(i)].data(), size_t(nc) * 8);
+        }
+        if (diag) {
+            const auto& d = r.diagnostics;
+            *diag = odegpu_scan_diagnostics{};
+            diag->detections = d.detections;
+            diag->detections_outside_zone = d.detections_outside_zone;
+            diag->max_residual_ratio = d.max_residual_ratio;
+            diag->secant_failures = d.secant_failures;
+            diag->nonfinite_systems = d.nonfinite_systems;
+            for (int k = 0; k < 4; ++k) diag->reason_counts[k] = d.reason_counts[static_cast<std::size_t>(k)];
+            diag->start_times_strictly_increase = d.start_times_strictly_increase ? 1 : 0;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return ODEGPU_ERR_INVALID_ARGUMENT;
+    }
+}
+
 } // extern "C"

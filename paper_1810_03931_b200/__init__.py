@@ -4,7 +4,7 @@ The compute path is libodegpu.so (hand-written sm_100a CUDA behind the C ABI
 in include/odegpu.h). This package is the thin host mirror used by tests and
 bench.py; the C++ host API lives in include/odegpu/.
 """
-from . import abi, models, workloads  # noqa: F401
+from . import abi, models, scan, workloads  # noqa: F401
 from .api import (  # noqa: F401
     BatchDims,
     CopyMode,

@@ -199,6 +199,53 @@ class LibraryMissing(RuntimeError):
     pass
 
 
+# ---- scan protocols (include/odegpu.h: odegpu_scan_run)
+SCAN_DUFFING_POINCARE, SCAN_DUFFING_MAXIMA_ACCESSORY, SCAN_DUFFING_MAXIMA_EVENT = 0, 1, 2
+SCAN_DUFFING_LYAPUNOV, SCAN_BUBBLE, SCAN_VALVE = 3, 4, 5
+
+
+class ParamRangeC(C.Structure):
+    _fields_ = [("min", C.c_double), ("max", C.c_double), ("res", Index), ("log_scale", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class ScanOptions(C.Structure):
+    _fields_ = [("algorithm", C.c_int32), ("device", C.c_int32), ("dt", C.c_double), ("rel_tol", C.c_double),
+                ("abs_tol", C.c_double), ("event_tol", C.c_double), ("batch_capacity", Index)]
+
+
+class DuffingScanC(C.Structure):
+    _fields_ = [("k", ParamRangeC), ("forcing_amplitude", C.c_double), ("stiffness", C.c_double),
+                ("forcing_omega", C.c_double), ("ic", C.c_double * 2), ("transient", Index), ("saved", Index),
+                ("solver", ScanOptions)]
+
+
+class BubbleScanC(C.Structure):
+    _fields_ = [("pa1_bar", ParamRangeC), ("pa2_bar", ParamRangeC), ("f1_khz", ParamRangeC), ("f2_khz", ParamRangeC),
+                ("R_E", C.c_double), ("c_L", C.c_double), ("rho_L", C.c_double), ("P_inf", C.c_double),
+                ("p_V", C.c_double), ("sigma", C.c_double), ("mu_L", C.c_double), ("gamma", C.c_double),
+                ("theta", C.c_double), ("ic", C.c_double * 2), ("t_end", C.c_double), ("transient", Index),
+                ("saved", Index), ("solver", ScanOptions)]
+
+
+class ValveScanC(C.Structure):
+    _fields_ = [("q", ParamRangeC), ("kappa", C.c_double), ("delta", C.c_double), ("beta", C.c_double),
+                ("restitution", C.c_double), ("ic", C.c_double * 3), ("t_end", C.c_double), ("transient", Index),
+                ("saved", Index), ("solver", ScanOptions)]
+
+
+class ScanDiagnosticsC(C.Structure):
+    _fields_ = [("detections", Index), ("detections_outside_zone", Index), ("max_residual_ratio", C.c_double),
+                ("secant_failures", Index), ("nonfinite_systems", Index), ("reason_counts", Index * 4),
+                ("start_times_strictly_increase", C.c_int32), ("reserved", C.c_int32)]
+
+
+class ScanTally(C.Structure):
+    _fields_ = [("reason_counts", Index * 4), ("secant_failures", Index), ("detections", Index),
+                ("detections_outside_zone", Index), ("max_residual_ratio", C.c_double),
+                ("start_time_not_advanced", Index), ("nonfinite_systems", Index)]
+
+
 _lib = None
 
 
@@ -252,6 +299,14 @@ def _bind(lib):
              C.c_uint32, CHUNK_SINK, vp],
         ),
         "odegpu_pipeline_destroy": (None, [vp]),
+        "odegpu_pipeline_run_tallied": (
+            C.c_int,
+            [vp, P(PoolView), P(PoolOut), P(SolverConfig), P(OdeControls), P(EventControls), Index, Index,
+             C.c_uint32, CHUNK_SINK, vp, P(ScanTally)],
+        ),
+        "odegpu_scan_run": (C.c_int, [C.c_int32, vp, P(C.c_double), Index, P(Index), P(Index), P(ScanDiagnosticsC),
+                                      C.c_char_p]),
+        "odegpu_param_range_values": (C.c_int, [P(ParamRangeC), P(C.c_double)]),
         "odegpu_math_check": (C.c_int, [C.c_int, Index, vp, vp, vp, vp]),
         "odegpu_slice": (C.c_int, [Index, C.c_int, C.c_int, P(Index), P(Index)]),
         "odegpu_host_register": (C.c_int, [vp, C.c_size_t]),

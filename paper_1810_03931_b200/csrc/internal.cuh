@@ -108,6 +108,7 @@ void launch_scatter_rows(odegpu_batch* b, Real* dst, const Index* d_idx, const R
                          Index components);
 void enqueue_time_check(odegpu_batch* b); // solve.hpp:159-161 on [0, a.count)
 void launch_diagnostics(odegpu_batch* b);
+void launch_tally(odegpu_batch* b, unsigned long long* tally, bool chunk_end); // scan outcome tally
 double run_dfma_peak(int blocks, int threads, int iters, double* seconds);
 
 // ---- model translation units: widths and kernel dispatch per model family

@@ -4,6 +4,7 @@
 // per device; no inter-GPU traffic: systems are independent).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <mutex>
@@ -150,6 +151,7 @@ struct Run {
     odegpu_chunk_sink sink;
     void* user;
     std::mutex* sink_mutex; // serialises sinks across device threads
+    odegpu_scan_tally* tally = nullptr; // scan tallies, merged under sink_mutex
 };
 
 } // namespace
@@ -164,6 +166,8 @@ struct odegpu_pipeline {
     Index rec_capacity = 0; // recorded iterations the staging can hold
     odegpu::detail::Slot slots[2];
     std::vector<odegpu_outcome> packed;
+    unsigned long long* d_tally = nullptr; // device scan tally (kTallySlots counters)
+    unsigned long long* h_tally = nullptr; // pinned mirror
 
     ~odegpu_pipeline() {
         for (auto& s : slots) {
@@ -178,6 +182,8 @@ struct odegpu_pipeline {
             if (s.d_packed) cudaFree(s.d_packed);
             for (auto& o : s.rec_out) o.release();
         }
+        if (d_tally) cudaFree(d_tally);
+        if (h_tally) cudaFreeHost(h_tally);
     }
 };
 
@@ -204,6 +210,8 @@ odegpu_pipeline* pipeline_create(const odegpu_model& model, Index capacity, int 
             CK(cudaMallocHost(&s.fin_out, size_t(capacity) * sizeof(odegpu_outcome)));
             CK(cudaMalloc(&s.d_packed, size_t(capacity) * sizeof(odegpu_outcome)));
         }
+        CK(cudaMalloc(&p->d_tally, dev::kTallySlots * sizeof(unsigned long long)));
+        CK(cudaMallocHost(&p->h_tally, dev::kTallySlots * sizeof(unsigned long long)));
     } catch (...) {
         delete p;
         throw;
@@ -250,6 +258,13 @@ void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
     const Index N = pd.problem_size;
     const bool r_td = mask & 1u, r_y = mask & 2u, r_acc = (mask & 8u) && sd.accessory_count, r_out = mask & 16u;
     DeviceGuard g(p->device);
+    unsigned long long* tally = j.tally ? p->d_tally : nullptr;
+    if (tally) { // zeroed on slot 0's stream, ordered before slot 1's first kernel
+        CK(cudaMemsetAsync(tally, 0, dev::kTallySlots * sizeof(unsigned long long), p->slots[0].batch->stream));
+        CK(cudaEventRecord(p->slots[0].done, p->slots[0].batch->stream));
+        CK(cudaStreamWaitEvent(p->slots[1].batch->stream, p->slots[0].done, 0));
+    }
+    for (auto& s : p->slots) s.batch->a.tally = tally;
     if (n_rec > 0) {
         // (re)allocate when the mask needs arrays the staging lacks
         const Slot& s0 = p->slots[0];
@@ -282,7 +297,7 @@ void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
         if (o.state && !d_y) put(o.state, s.fin_y, sd.system_dim);
         if (o.accessories && sd.accessory_count && !d_acc) put(o.accessories, s.fin_acc, sd.accessory_count);
         if (o.outcomes && !d_out) std::memcpy(o.outcomes + off, s.fin_out, size_t(n) * sizeof(odegpu_outcome));
-        if (j.sink && n_rec > 0) {
+        if (j.sink) { // also with no recorded iteration (n_rec = 0): the chunk is done
             if (r_out)
                 for (Index r = 0; r < n_rec; ++r) s.rec_out[size_t(r)].pack(p->packed.data() + r * n, n);
             // compact the recorded arrays from stride cap to stride n
@@ -328,6 +343,7 @@ void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
             for (Index it = 0; it < j.iterations; ++it) {
                 enqueue_time_check(b);
                 launch_model(b, p->model, j.cfg->algorithm, c);
+                if (tally) launch_tally(b, tally, false);
                 if (n_rec > 0 && it >= j.record_from) {
                     const Index r = it - j.record_from;
                     if (r_td) copy_d2h_strided(s.rec_td + r * 2 * cap, cap, 0, b->a.td, cap, 0, n, 2, b->stream);
@@ -340,6 +356,7 @@ void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
                     if (r_out) s.rec_out[size_t(r)].fetch(b, 0, n, b->stream);
                 }
             }
+            if (tally) launch_tally(b, tally, true);
             if (o.time_domain) {
                 if (d_td) copy_d2h_strided(o.time_domain, N, start, b->a.td, cap, 0, n, 2, b->stream);
                 else copy_d2h_strided(s.fin_td, cap, 0, b->a.td, cap, 0, n, 2, b->stream);
@@ -370,7 +387,24 @@ void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
         }
         drain(p->slots[k & 1]); // oldest first
         drain(p->slots[(k + 1) & 1]);
+        if (tally) { // both slot streams are drained: merge the device tally
+            CK(cudaMemcpy(p->h_tally, tally, dev::kTallySlots * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+            const unsigned long long* h = p->h_tally;
+            std::lock_guard<std::mutex> lock(*j.sink_mutex);
+            odegpu_scan_tally& t = *j.tally;
+            for (int r = 0; r < 4; ++r) t.reason_counts[r] += Index(h[dev::kTallyReason0 + r]);
+            t.secant_failures += Index(h[dev::kTallySecantFailures]);
+            t.detections += Index(h[dev::kTallyDetections]);
+            t.detections_outside_zone += Index(h[dev::kTallyOutsideZone]);
+            double mr = 0;
+            std::memcpy(&mr, h + dev::kTallyMaxRatio, sizeof mr);
+            t.max_residual_ratio = std::max(t.max_residual_ratio, mr);
+            t.start_time_not_advanced += Index(h[dev::kTallyStartNotAdvanced]);
+            t.nonfinite_systems += Index(h[dev::kTallyNonfinite]);
+        }
+        for (auto& s : p->slots) s.batch->a.tally = nullptr;
     } catch (...) {
+        for (auto& s : p->slots) s.batch->a.tally = nullptr;
         for (auto& s : p->slots) {
             if (s.batch) cudaStreamSynchronize(s.batch->stream);
             s.busy = false;
@@ -441,6 +475,21 @@ int odegpu_pipeline_run(odegpu_pipeline* p, const odegpu_pool_view* pool, const 
         validate_run(pool, cfg, ode, iterations, record_from);
         std::mutex mu;
         const Run j{pool, out, cfg, ode, ev, iterations, record_from, record_mask, on_chunk, user, &mu};
+        run_range(p, j, 0, pool->dims.problem_size);
+    });
+}
+
+int odegpu_pipeline_run_tallied(odegpu_pipeline* p, const odegpu_pool_view* pool, const odegpu_pool_out* out,
+                                const odegpu_solver_config* cfg, const odegpu_ode_controls* ode,
+                                const odegpu_event_controls* ev, odegpu_index iterations, odegpu_index record_from,
+                                uint32_t record_mask, odegpu_chunk_sink on_chunk, void* user,
+                                odegpu_scan_tally* tally) {
+    return guarded([&] {
+        if (!p || !tally) throw_invalid("null argument");
+        validate_run(pool, cfg, ode, iterations, record_from);
+        std::mutex mu;
+        Run j{pool, out, cfg, ode, ev, iterations, record_from, record_mask, on_chunk, user, &mu};
+        j.tally = tally;
         run_range(p, j, 0, pool->dims.problem_size);
     });
 }

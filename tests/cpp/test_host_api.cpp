@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "odegpu/odegpu.hpp"
+#include "odegpu/scan.hpp"
 
 using namespace odegpu;
 
@@ -322,6 +323,66 @@ int main() {
         });
         CHECK(models::lyapunov_accumulate(samples[0], kTwoPi) < 0.0);
         CHECK(models::lyapunov_accumulate(samples[1], kTwoPi) > 0.0);
+    });
+
+    run_case("scan protocols: rows, order, diagnostics, CSV (scan.hpp)", [] { // test_scan.cpp:49-131
+        scan::DuffingScanSpec spec;
+        spec.k = scan::ParamRange{0.2, 0.3, 24, scan::Scale::Linear};
+        spec.transient = 3;
+        spec.saved = 2;
+        spec.solver.batch_capacity = 10; // 3 chunks
+        const auto acc = scan::run_duffing_maxima(spec, scan::MaximaMode::Accessory);
+        CHECK(acc.columns == std::vector<std::string>({"k", "y1_max", "status"}));
+        CHECK(acc.rows.size() == 48);
+        CHECK(acc.rows[0][0] == 0.2 && acc.rows[9][0] == spec.k.values()[9]); // chunk-major, iteration, system
+        CHECK(acc.diagnostics.reason_counts[0] == 24 * 5);
+        // test_scan.cpp:132-159: on a converged periodic window both
+        // recordings agree on the envelope over the saved iterations
+        scan::DuffingScanSpec w;
+        w.k = scan::ParamRange{0.21, 0.22, 3, scan::Scale::Linear};
+        w.transient = 512;
+        w.saved = 4;
+        const auto wa = scan::run_duffing_maxima(w, scan::MaximaMode::Accessory);
+        const auto ev = scan::run_duffing_maxima(w, scan::MaximaMode::Event);
+        CHECK(wa.rows.size() == 12 && ev.rows.size() == 12);
+        CHECK(wa.diagnostics.detections == 0);
+        CHECK(ev.diagnostics.detections > 0);
+        CHECK(ev.diagnostics.detections_outside_zone == 0);
+        CHECK(ev.diagnostics.max_residual_ratio > 0 && ev.diagnostics.max_residual_ratio <= 1.0);
+        for (std::size_t k = 0; k < 3; ++k) {
+            Real env_acc = -1e300, env_evt = -1e300;
+            for (std::size_t i = 0; i < 4; ++i) {
+                env_acc = std::max(env_acc, wa.rows[3 * i + k][1]);
+                env_evt = std::max(env_evt, ev.rows[3 * i + k][1]);
+            }
+            // doctest::Approx(env_evt).epsilon(1e-4): eps * (scale 1 + max magnitude)
+            CHECK(std::abs(env_acc - env_evt) < 1e-4 * (1.0 + std::max(std::abs(env_acc), std::abs(env_evt))));
+        }
+        scan::BubbleScanSpec b;
+        b.f1_khz = scan::ParamRange{20.0, 1000.0, 3, scan::Scale::Log};
+        b.f2_khz = scan::ParamRange{20.0, 1000.0, 3, scan::Scale::Log};
+        b.transient = 4;
+        b.saved = 4;
+        const auto br = scan::run_bubble_scan(b);
+        CHECK(br.rows.size() == 9);
+        CHECK(br.diagnostics.reason_counts[1] == 72); // test_scan.cpp:195
+        CHECK(br.diagnostics.start_times_strictly_increase);
+        const std::string path = "/tmp/odegpu_scan_test.csv";
+        scan::emit_rows(path, acc.columns, acc.rows);
+        std::FILE* f = std::fopen(path.c_str(), "r");
+        CHECK(f != nullptr);
+        char line[256];
+        CHECK(std::fgets(line, sizeof line, f) && std::string(line) == "# k,y1_max,status\n");
+        double k = 0, y = 0, st = 0;
+        CHECK(std::fscanf(f, "%lf,%lf,%lf", &k, &y, &st) == 3 && k == acc.rows[0][0] && y == acc.rows[0][1]);
+        std::fclose(f);
+        bool threw = false;
+        try {
+            scan::ParamRange{0.0, 1.0, 4, scan::Scale::Log}.values();
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
     });
 
     std::printf("%d checks, %d failed\n", g_checks, g_failed);
