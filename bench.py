@@ -15,9 +15,10 @@ the local-maximum EventFunction and event-time accessories on a 1024 x 1024
   batch's stream around each solve, L2 flushed (256 MiB write) between steps
   outside the events.
 * e2e: the same metric through the C ABI with host (pinned) buffers: the
-  chunked pool pipeline (odegpu_pipeline_run, 4 chunks) — H2D of the pool,
-  solve, D2H of time domains / state / accessories / outcome records into
-  host arrays, per step, wall-clock.
+  chunked pool pipeline (odegpu_pipeline_run, 8 chunks, copy-in / kernels /
+  copy-out streams overlapped) — H2D of the pool, solve, D2H of time
+  domains / state / accessories / outcome records into host arrays, per
+  step, wall-clock.
 * roofline: FP64-pipe lane instructions per trial step (SURVEY.md §8d
   algorithmic count) / solve-kernel time vs the DFMA microbenchmark peak.
 * cpu_baseline: the reference solver (oracle/_ref, compiled from the
@@ -331,10 +332,11 @@ def main():
         abi.OUTCOME_DTYPE)
     if world > 1:
         torch.distributed.barrier()
-    # the chunked pool pipeline: 4 chunks, H2D of chunk k+1 and D2H of chunk
-    # k-1 overlap chunk k's kernels (odegpu_pipeline_run); device batches and
-    # pinned staging are allocated once, like a scan driver would
-    cap = max(1, n // 4)
+    # the chunked pool pipeline: 8 chunks through a 3-stage copy-in /
+    # kernels / copy-out pipeline (odegpu_pipeline_run; 8 measured best of
+    # 4-16, scripts/e2e_chunks.py); device batches and pinned staging are
+    # allocated once, like a scan driver would
+    cap = max(1, n // 8)
     pipe = pkg.api.Pipeline(wl.model, cap, device)
     outs = (o_td, o_y, o_a, outc)
     pipe.run(pin_pool, cfg, 1, out_arrays=outs)  # warm-up (first-touch of the output pages)
@@ -415,8 +417,9 @@ def main():
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "steps": args.e2e_steps,
-                "path": "odegpu_solve_pool over the pinned host pool: 4 chunks, double-buffered H2D / solve / "
-                        "D2H of td, state, accessories and outcomes into host arrays, wall-clock"},
+                "path": "odegpu_pipeline_run over the pinned host pool: 8 chunks, H2D / kernels / D2H of td, "
+                        "state, accessories and outcome records on separate streams (4 chunks in flight), "
+                        "into host arrays, wall-clock"},
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
     }

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <mutex>
@@ -125,8 +127,10 @@ double* pinned(Index doubles) {
 
 /// One half of the double buffer: a device batch plus pinned staging.
 struct Slot {
-    odegpu_batch* batch = nullptr;
-    cudaEvent_t done = nullptr;
+    odegpu_batch* batch = nullptr; // compute runs on batch->stream
+    cudaEvent_t loaded = nullptr;   // H2D of the slot's chunk done (copy-in stream)
+    cudaEvent_t computed = nullptr; // kernels of the chunk done (compute stream)
+    cudaEvent_t done = nullptr;     // D2H of the chunk done (copy-out stream)
     double* fin_td = nullptr; // endpoints of the chunk, [comps][cap]
     double* fin_y = nullptr;
     double* fin_acc = nullptr;
@@ -164,7 +168,9 @@ struct odegpu_pipeline {
     Index cap = 0;
     int device = 0;
     Index rec_capacity = 0; // recorded iterations the staging can hold
-    odegpu::detail::Slot slots[2];
+    static constexpr int kSlots = 4; // chunks in flight: copy-in, compute (two), copy-out
+    odegpu::detail::Slot slots[kSlots];
+    cudaStream_t copy_in = nullptr, copy_out = nullptr;
     std::vector<odegpu_outcome> packed;
     unsigned long long* d_tally = nullptr; // device scan tally (kTallySlots counters)
     unsigned long long* h_tally = nullptr; // pinned mirror
@@ -175,13 +181,19 @@ struct odegpu_pipeline {
                 cudaStreamSynchronize(s.batch->stream);
                 odegpu_batch_destroy(s.batch);
             }
-            if (s.done) cudaEventDestroy(s.done);
+            for (cudaEvent_t e : {s.loaded, s.computed, s.done})
+                if (e) cudaEventDestroy(e);
             for (double* p : {s.fin_td, s.fin_y, s.fin_acc, s.rec_td, s.rec_y, s.rec_acc})
                 if (p) cudaFreeHost(p);
             if (s.fin_out) cudaFreeHost(s.fin_out);
             if (s.d_packed) cudaFree(s.d_packed);
             for (auto& o : s.rec_out) o.release();
         }
+        for (cudaStream_t st : {copy_in, copy_out})
+            if (st) {
+                cudaStreamSynchronize(st);
+                cudaStreamDestroy(st);
+            }
         if (d_tally) cudaFree(d_tally);
         if (h_tally) cudaFreeHost(h_tally);
     }
@@ -201,9 +213,12 @@ odegpu_pipeline* pipeline_create(const odegpu_model& model, Index capacity, int 
         DeviceGuard g(device);
         const auto& sd = p->sd;
         const odegpu_batch_dims bd{capacity, sd.system_dim, sd.param_count, sd.event_count, sd.accessory_count};
+        CK(cudaStreamCreateWithFlags(&p->copy_in, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&p->copy_out, cudaStreamNonBlocking));
         for (auto& s : p->slots) {
             s.batch = batch_create(bd, device);
-            CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+            for (cudaEvent_t* e : {&s.loaded, &s.computed, &s.done})
+                CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
             s.fin_td = pinned(2 * capacity);
             s.fin_y = pinned(sd.system_dim * capacity);
             s.fin_acc = pinned(sd.accessory_count * capacity);
@@ -259,11 +274,8 @@ void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
     const bool r_td = mask & 1u, r_y = mask & 2u, r_acc = (mask & 8u) && sd.accessory_count, r_out = mask & 16u;
     DeviceGuard g(p->device);
     unsigned long long* tally = j.tally ? p->d_tally : nullptr;
-    if (tally) { // zeroed on slot 0's stream, ordered before slot 1's first kernel
-        CK(cudaMemsetAsync(tally, 0, dev::kTallySlots * sizeof(unsigned long long), p->slots[0].batch->stream));
-        CK(cudaEventRecord(p->slots[0].done, p->slots[0].batch->stream));
-        CK(cudaStreamWaitEvent(p->slots[1].batch->stream, p->slots[0].done, 0));
-    }
+    // zeroed on the copy-in stream: every chunk's kernels wait for its H2D
+    if (tally) CK(cudaMemsetAsync(tally, 0, dev::kTallySlots * sizeof(unsigned long long), p->copy_in));
     for (auto& s : p->slots) s.batch->a.tally = tally;
     if (n_rec > 0) {
         // (re)allocate when the mask needs arrays the staging lacks
@@ -321,30 +333,52 @@ void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
         }
     };
 
+    // ODEGPU_PIPELINE_TRACE=1: per-chunk CUDA-event timeline on stderr
+    static const bool trace = std::getenv("ODEGPU_PIPELINE_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t st) {
+        if (!trace) return;
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(e, st));
+        tev.push_back(e);
+    };
+    // Three-stage pipeline over kSlots device batches: chunk k's H2D runs on
+    // the copy-in stream, its kernels on the slot batch's stream (after the
+    // H2D event), its D2H on the copy-out stream (after the kernels' event),
+    // so H2D(k+1), the kernels of k and D2H(k-1) overlap (PCIe is full
+    // duplex: 55 GB/s each way measured on the B200 box, 99 GB/s both). A
+    // slot is refilled only after its previous chunk was drained on the host.
+    constexpr int kSlots = odegpu_pipeline::kSlots;
     int k = 0;
     try {
         for (Index start = begin; start < end; start += cap, ++k) {
-            Slot& s = p->slots[k & 1];
+            Slot& s = p->slots[k % kSlots];
             drain(s); // the slot's previous chunk must be consumed before reuse
             odegpu_batch* b = s.batch;
+            mark(p->copy_in);
             const Index n = std::min(cap, end - start);
             s.start = start;
             s.count = n;
             b->a.count = n;
-            // linear_set(All) of the chunk: pool -> batch, fresh outcomes (batch.cpp:78-104)
-            copy_h2d_strided(b->a.td, cap, 0, j.pool->time_domain, N, start, n, 2, b->stream);
-            copy_h2d_strided(b->a.state, cap, 0, j.pool->state, N, start, n, sd.system_dim, b->stream);
+            // linear_set(All) of the chunk: pool -> batch (batch.cpp:78-104), on the copy-in stream
+            copy_h2d_strided(b->a.td, cap, 0, j.pool->time_domain, N, start, n, 2, p->copy_in);
+            copy_h2d_strided(b->a.state, cap, 0, j.pool->state, N, start, n, sd.system_dim, p->copy_in);
             if (sd.param_count)
                 copy_h2d_strided(const_cast<Real*>(b->a.params), cap, 0, j.pool->parameters, N, start, n,
-                                 sd.param_count, b->stream);
+                                 sd.param_count, p->copy_in);
             if (sd.accessory_count)
-                copy_h2d_strided(b->a.acc, cap, 0, j.pool->accessories, N, start, n, sd.accessory_count, b->stream);
+                copy_h2d_strided(b->a.acc, cap, 0, j.pool->accessories, N, start, n, sd.accessory_count, p->copy_in);
+            CK(cudaEventRecord(s.loaded, p->copy_in));
+            // kernels: fresh outcomes, then every iteration back to back
+            CK(cudaStreamWaitEvent(b->stream, s.loaded, 0));
+            mark(b->stream);
             launch_reset_outcomes(b, 0, n);
             for (Index it = 0; it < j.iterations; ++it) {
                 enqueue_time_check(b);
                 launch_model(b, p->model, j.cfg->algorithm, c);
                 if (tally) launch_tally(b, tally, false);
-                if (n_rec > 0 && it >= j.record_from) {
+                if (n_rec > 0 && it >= j.record_from) { // snapshots stay ordered with the kernels
                     const Index r = it - j.record_from;
                     if (r_td) copy_d2h_strided(s.rec_td + r * 2 * cap, cap, 0, b->a.td, cap, 0, n, 2, b->stream);
                     if (r_y)
@@ -357,36 +391,51 @@ void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
                 }
             }
             if (tally) launch_tally(b, tally, true);
-            if (o.time_domain) {
-                if (d_td) copy_d2h_strided(o.time_domain, N, start, b->a.td, cap, 0, n, 2, b->stream);
-                else copy_d2h_strided(s.fin_td, cap, 0, b->a.td, cap, 0, n, 2, b->stream);
-            }
-            if (o.state) {
-                if (d_y) copy_d2h_strided(o.state, N, start, b->a.state, cap, 0, n, sd.system_dim, b->stream);
-                else copy_d2h_strided(s.fin_y, cap, 0, b->a.state, cap, 0, n, sd.system_dim, b->stream);
-            }
-            if (o.accessories && sd.accessory_count) {
-                if (d_acc)
-                    copy_d2h_strided(o.accessories, N, start, b->a.acc, cap, 0, n, sd.accessory_count, b->stream);
-                else
-                    copy_d2h_strided(s.fin_acc, cap, 0, b->a.acc, cap, 0, n, sd.accessory_count, b->stream);
-            }
             if (o.outcomes) {
                 pack_outcomes_kernel<<<grid_for(b, n, 256), 256, 0, b->stream>>>(b->a, n, s.d_packed);
                 CK(cudaGetLastError());
                 ++b->launches;
-                CK(cudaMemcpyAsync(d_out ? o.outcomes + start : s.fin_out, s.d_packed,
-                                   size_t(n) * sizeof(odegpu_outcome), cudaMemcpyDeviceToHost, b->stream));
             }
-            CK(cudaMemcpyAsync(b->host_flag, b->first_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                               b->stream));
-            CK(cudaEventRecord(s.done, b->stream));
+            CK(cudaEventRecord(s.computed, b->stream));
+            // endpoints on the copy-out stream
+            CK(cudaStreamWaitEvent(p->copy_out, s.computed, 0));
+            mark(p->copy_out);
+            cudaStream_t out_s = p->copy_out;
+            if (o.time_domain) {
+                if (d_td) copy_d2h_strided(o.time_domain, N, start, b->a.td, cap, 0, n, 2, out_s);
+                else copy_d2h_strided(s.fin_td, cap, 0, b->a.td, cap, 0, n, 2, out_s);
+            }
+            if (o.state) {
+                if (d_y) copy_d2h_strided(o.state, N, start, b->a.state, cap, 0, n, sd.system_dim, out_s);
+                else copy_d2h_strided(s.fin_y, cap, 0, b->a.state, cap, 0, n, sd.system_dim, out_s);
+            }
+            if (o.accessories && sd.accessory_count) {
+                if (d_acc)
+                    copy_d2h_strided(o.accessories, N, start, b->a.acc, cap, 0, n, sd.accessory_count, out_s);
+                else
+                    copy_d2h_strided(s.fin_acc, cap, 0, b->a.acc, cap, 0, n, sd.accessory_count, out_s);
+            }
+            if (o.outcomes)
+                CK(cudaMemcpyAsync(d_out ? o.outcomes + start : s.fin_out, s.d_packed,
+                                   size_t(n) * sizeof(odegpu_outcome), cudaMemcpyDeviceToHost, out_s));
+            CK(cudaMemcpyAsync(b->host_flag, b->first_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, out_s));
+            mark(out_s);
+            CK(cudaEventRecord(s.done, out_s));
             s.busy = true;
-            // chunk k-1 (the other slot) is drained at the top of the next
-            // iteration, so its D2H and host work overlap chunk k's kernels
         }
-        drain(p->slots[k & 1]); // oldest first
-        drain(p->slots[(k + 1) & 1]);
+        for (int r = 0; r < kSlots; ++r) drain(p->slots[(k + r) % kSlots]); // oldest first
+        if (trace && !tev.empty()) {
+            for (size_t c = 0; c + 3 < tev.size(); c += 4) {
+                float a = 0, h = 0, x = 0, d = 0;
+                cudaEventElapsedTime(&a, tev[0], tev[c]);
+                cudaEventElapsedTime(&h, tev[c], tev[c + 1]);
+                cudaEventElapsedTime(&x, tev[c + 1], tev[c + 2]);
+                cudaEventElapsedTime(&d, tev[c + 2], tev[c + 3]);
+                std::fprintf(stderr, "[pipeline] chunk %zu: h2d at %.3f ms, +%.3f to kernels, +%.3f to d2h, d2h %.3f\n",
+                             c / 4, a, h, x, d);
+            }
+            for (auto e : tev) cudaEventDestroy(e);
+        }
         if (tally) { // both slot streams are drained: merge the device tally
             CK(cudaMemcpy(p->h_tally, tally, dev::kTallySlots * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
             const unsigned long long* h = p->h_tally;
