@@ -80,6 +80,9 @@ struct SolveOptions {
     Index tile_size = 64;
     Index batch_capacity = 0;
     int device = 0;
+    /// More than one entry: the chunks are spread over these devices (whole
+    /// chunks, pool order — rows and diagnostics equal the one-device run's).
+    std::vector<int> devices{};
 };
 
 /// scan.hpp:41-49
@@ -193,34 +196,40 @@ struct Chunk {
 
 /// run_chunks (src/scan.cpp:88-112) on the device pipeline: the pool in
 /// chunks of batch_capacity systems, transient + saved iterations per chunk,
-/// on_chunk(Chunk) with the saved iterations' records; the tallies go to
+/// on_chunk(Chunk, rows) with the saved iterations' records appends the
+/// chunk's rows; chunks may finish out of order on several devices, so rows
+/// are gathered per chunk and concatenated in pool order. The tallies go to
 /// `diag`.
+using Rows = std::vector<std::vector<Real>>;
+
 template <SystemModel D, class OnChunk>
 void run_chunks(const D& def, const ProblemPool& pool, const SolveOptions& opt, Index transient, Index saved,
-                uint32_t record_mask, ScanDiagnostics& diag, OnChunk&& on_chunk, bool check_start_times = false) {
+                uint32_t record_mask, ScanResult& result, OnChunk&& on_chunk, bool check_start_times = false) {
     const Index n_pool = pool.size();
     const Index cap = opt.batch_capacity > 0 ? std::min(opt.batch_capacity, n_pool) : n_pool;
     const SolverConfig cfg{opt.algorithm, opt.dt, opt.tile_size, opt.workers};
     odegpu::detail::CControls cc(def, cfg);
     const odegpu_model m = def.descriptor();
-    odegpu_pipeline* pipe = nullptr;
-    odegpu::detail::check(odegpu_pipeline_create(&m, cap, opt.device, &pipe));
     std::vector<odegpu_outcome> final_outcomes(static_cast<std::size_t>(n_pool));
     odegpu_pool_out out{};
     out.outcomes = final_outcomes.data();
+    std::vector<Rows> chunk_rows(static_cast<std::size_t>((n_pool + cap - 1) / cap));
     struct Ctx {
         OnChunk* f;
         const odegpu_outcome* fin;
-        Index dim, acc;
+        Index dim, acc, cap;
+        std::vector<Rows>* rows;
         std::exception_ptr err;
-    } ctx{&on_chunk, final_outcomes.data(), def.dims().system_dim, def.dims().accessory_count, nullptr};
-    // The final outcomes of chunk k land in `out` before chunk k's sink runs
-    // (the pipeline drains a slot — endpoint D2H first — then calls the sink).
+    } ctx{&on_chunk, final_outcomes.data(), def.dims().system_dim, def.dims().accessory_count, cap, &chunk_rows,
+          nullptr};
+    // A chunk's final outcomes land in `out` before its sink runs (the
+    // pipeline drains a slot — endpoint D2H first — then calls the sink).
     auto sink = [](odegpu_index start, odegpu_index count, odegpu_index n_rec, const odegpu_chunk_record* rec,
                    void* user) -> int {
         auto* c = static_cast<Ctx*>(user);
         try {
-            (*c->f)(Chunk{start, count, n_rec, rec, c->fin, c->dim, c->acc});
+            (*c->f)(Chunk{start, count, n_rec, rec, c->fin, c->dim, c->acc},
+                    (*c->rows)[static_cast<std::size_t>(start / c->cap)]);
         } catch (...) {
             c->err = std::current_exception();
             return ODEGPU_ERR_INVALID_ARGUMENT;
@@ -229,11 +238,23 @@ void run_chunks(const D& def, const ProblemPool& pool, const SolveOptions& opt, 
     };
     odegpu_scan_tally t{};
     const odegpu_pool_view v = pool.view();
-    const int rc = odegpu_pipeline_run_tallied(pipe, &v, &out, &cc.c_cfg, &cc.c_ode, &cc.c_ev, transient + saved,
-                                               transient, record_mask | kRecOutcomes, sink, &ctx, &t);
-    odegpu_pipeline_destroy(pipe);
+    int rc = 0;
+    if (opt.devices.size() > 1) {
+        rc = odegpu_solve_pool_multi_tallied(&v, &out, &m, &cc.c_cfg, &cc.c_ode, &cc.c_ev, cap, transient + saved,
+                                             transient, record_mask | kRecOutcomes, sink, &ctx, opt.devices.data(),
+                                             static_cast<int>(opt.devices.size()), 1, &t);
+    } else {
+        odegpu_pipeline* pipe = nullptr;
+        odegpu::detail::check(odegpu_pipeline_create(&m, cap, opt.devices.empty() ? opt.device : opt.devices[0], &pipe));
+        rc = odegpu_pipeline_run_tallied(pipe, &v, &out, &cc.c_cfg, &cc.c_ode, &cc.c_ev, transient + saved, transient,
+                                         record_mask | kRecOutcomes, sink, &ctx, &t);
+        odegpu_pipeline_destroy(pipe);
+    }
     if (ctx.err) std::rethrow_exception(ctx.err);
     odegpu::detail::check(rc);
+    for (auto& r : chunk_rows)
+        for (auto& row : r) result.rows.push_back(std::move(row));
+    ScanDiagnostics& diag = result.diagnostics;
     diag.detections += t.detections;
     diag.detections_outside_zone += t.detections_outside_zone;
     diag.max_residual_ratio = std::max(diag.max_residual_ratio, t.max_residual_ratio);
@@ -282,11 +303,11 @@ inline ScanResult run_duffing_poincare(const DuffingScanSpec& spec) {
     models::DuffingSystem def(OdeControls::uniform(2, spec.solver.rel_tol, spec.solver.abs_tol));
     ScanResult result;
     result.columns = {"k", "B", "y1", "y2", "status"};
-    detail::run_chunks(def, pool, spec.solver, spec.transient, spec.saved, detail::kRecState, result.diagnostics,
-                       [&](const detail::Chunk& c) {
+    detail::run_chunks(def, pool, spec.solver, spec.transient, spec.saved, detail::kRecState, result,
+                       [&](const detail::Chunk& c, detail::Rows& rows) {
                            for (Index r = 0; r < c.n_saved; ++r)
                                for (Index s = 0; s < c.count; ++s)
-                                   result.rows.push_back({ks[static_cast<std::size_t>(c.start + s)],
+                                   rows.push_back({ks[static_cast<std::size_t>(c.start + s)],
                                                           spec.forcing_amplitude, c.state(r, s, 0), c.state(r, s, 1),
                                                           detail::status(c.aborted(r, s))});
                        });
@@ -303,11 +324,11 @@ inline ScanResult run_duffing_maxima(const DuffingScanSpec& spec, MaximaMode mod
     ScanResult result;
     result.columns = {"k", "y1_max", "status"};
     const auto collect = [&](const auto& def) {
-        detail::run_chunks(def, pool, spec.solver, spec.transient, spec.saved, detail::kRecAcc, result.diagnostics,
-                           [&](const detail::Chunk& c) {
+        detail::run_chunks(def, pool, spec.solver, spec.transient, spec.saved, detail::kRecAcc, result,
+                           [&](const detail::Chunk& c, detail::Rows& rows) {
                                for (Index r = 0; r < c.n_saved; ++r)
                                    for (Index s = 0; s < c.count; ++s)
-                                       result.rows.push_back({ks[static_cast<std::size_t>(c.start + s)],
+                                       rows.push_back({ks[static_cast<std::size_t>(c.start + s)],
                                                               c.acc(r, s, 0), detail::status(c.aborted(r, s))});
                            });
     };
@@ -329,8 +350,8 @@ inline ScanResult run_duffing_lyapunov(const DuffingScanSpec& spec) {
     models::DuffingLyapunovSystem def(OdeControls::uniform(4, spec.solver.rel_tol, spec.solver.abs_tol));
     ScanResult result;
     result.columns = {"k", "lambda_max", "status"};
-    detail::run_chunks(def, pool, spec.solver, spec.transient, spec.saved, detail::kRecAcc, result.diagnostics,
-                       [&](const detail::Chunk& c) {
+    detail::run_chunks(def, pool, spec.solver, spec.transient, spec.saved, detail::kRecAcc, result,
+                       [&](const detail::Chunk& c, detail::Rows& rows) {
                            std::vector<Real> samples;
                            for (Index s = 0; s < c.count; ++s) {
                                samples.clear();
@@ -344,7 +365,7 @@ inline ScanResult run_duffing_lyapunov(const DuffingScanSpec& spec) {
                                    lambda = models::lyapunov_accumulate(samples, period);
                                else
                                    st = 1.0;
-                               result.rows.push_back({ks[static_cast<std::size_t>(c.start + s)], lambda, st});
+                               rows.push_back({ks[static_cast<std::size_t>(c.start + s)], lambda, st});
                            }
                        });
     detail::maybe_emit(result, spec.output);
@@ -389,8 +410,8 @@ inline ScanResult run_bubble_scan(const BubbleScanSpec& spec) {
                                      OdeControls::uniform(2, spec.solver.rel_tol, spec.solver.abs_tol));
     ScanResult result;
     result.columns = {"omega1_radps", "omega2_radps", "pa1_pa", "pa2_pa", "y_exp", "status"};
-    detail::run_chunks(def, pool, spec.solver, spec.transient, spec.saved, detail::kRecAcc, result.diagnostics,
-                       [&](const detail::Chunk& c) {
+    detail::run_chunks(def, pool, spec.solver, spec.transient, spec.saved, detail::kRecAcc, result,
+                       [&](const detail::Chunk& c, detail::Rows& rows) {
                            for (Index s = 0; s < c.count; ++s) {
                                Real yexp = -std::numeric_limits<Real>::infinity();
                                for (Index r = 0; r < c.n_saved; ++r)
@@ -401,7 +422,7 @@ inline ScanResult run_bubble_scan(const BubbleScanSpec& spec) {
                                    st = 1.0;
                                }
                                const GridPoint& g = grid[static_cast<std::size_t>(c.start + s)];
-                               result.rows.push_back({g.w1, g.w2, g.pa1, g.pa2, yexp, st});
+                               rows.push_back({g.w1, g.w2, g.pa1, g.pa2, yexp, st});
                            }
                        },
                        /*check_start_times=*/true);
@@ -430,11 +451,11 @@ inline ScanResult run_valve_scan(const ValveScanSpec& spec) {
     models::ValveSystem def(spec.solver.event_tol, OdeControls::uniform(3, spec.solver.rel_tol, spec.solver.abs_tol));
     ScanResult result;
     result.columns = {"q", "y1_max", "y1_min", "status"};
-    detail::run_chunks(def, pool, spec.solver, spec.transient, spec.saved, detail::kRecAcc, result.diagnostics,
-                       [&](const detail::Chunk& c) {
+    detail::run_chunks(def, pool, spec.solver, spec.transient, spec.saved, detail::kRecAcc, result,
+                       [&](const detail::Chunk& c, detail::Rows& rows) {
                            for (Index r = 0; r < c.n_saved; ++r)
                                for (Index s = 0; s < c.count; ++s)
-                                   result.rows.push_back({qs[static_cast<std::size_t>(c.start + s)], c.acc(r, s, 0),
+                                   rows.push_back({qs[static_cast<std::size_t>(c.start + s)], c.acc(r, s, 0),
                                                           c.acc(r, s, 1), detail::status(c.aborted(r, s))});
                        });
     detail::maybe_emit(result, spec.output);

@@ -211,7 +211,8 @@ class ParamRangeC(C.Structure):
 
 class ScanOptions(C.Structure):
     _fields_ = [("algorithm", C.c_int32), ("device", C.c_int32), ("dt", C.c_double), ("rel_tol", C.c_double),
-                ("abs_tol", C.c_double), ("event_tol", C.c_double), ("batch_capacity", Index)]
+                ("abs_tol", C.c_double), ("event_tol", C.c_double), ("batch_capacity", Index),
+                ("devices", C.POINTER(C.c_int32)), ("n_devices", C.c_int32), ("reserved", C.c_int32)]
 
 
 class DuffingScanC(C.Structure):
@@ -306,6 +307,11 @@ def _bind(lib):
         ),
         "odegpu_scan_run": (C.c_int, [C.c_int32, vp, P(C.c_double), Index, P(Index), P(Index), P(ScanDiagnosticsC),
                                       C.c_char_p]),
+        "odegpu_solve_pool_multi_tallied": (
+            C.c_int,
+            [P(PoolView), P(PoolOut), P(Model), P(SolverConfig), P(OdeControls), P(EventControls), Index, Index,
+             Index, C.c_uint32, CHUNK_SINK, vp, P(C.c_int), C.c_int, C.c_int, P(ScanTally)],
+        ),
         "odegpu_param_range_values": (C.c_int, [P(ParamRangeC), P(C.c_double)]),
         "odegpu_math_check": (C.c_int, [C.c_int, Index, vp, vp, vp, vp]),
         "odegpu_slice": (C.c_int, [Index, C.c_int, C.c_int, P(Index), P(Index)]),

@@ -570,18 +570,38 @@ int odegpu_solve_pool_multi(const odegpu_pool_view* pool, const odegpu_pool_out*
                             const odegpu_event_controls* ev, odegpu_index batch_capacity,
                             odegpu_index iterations, odegpu_index record_from, uint32_t record_mask,
                             odegpu_chunk_sink on_chunk, void* user, const int* devices, int n_devices) {
+    return odegpu_solve_pool_multi_tallied(pool, out, model, cfg, ode, ev, batch_capacity, iterations, record_from,
+                                           record_mask, on_chunk, user, devices, n_devices, 0, nullptr);
+}
+
+int odegpu_solve_pool_multi_tallied(const odegpu_pool_view* pool, const odegpu_pool_out* out,
+                                    const odegpu_model* model, const odegpu_solver_config* cfg,
+                                    const odegpu_ode_controls* ode, const odegpu_event_controls* ev,
+                                    odegpu_index batch_capacity, odegpu_index iterations, odegpu_index record_from,
+                                    uint32_t record_mask, odegpu_chunk_sink on_chunk, void* user,
+                                    const int* devices, int n_devices, int chunk_aligned, odegpu_scan_tally* tally) {
     return guarded([&] {
         if (!devices || n_devices < 1) throw_invalid("solve_pool_multi: no devices");
         if (!model) throw_invalid("solve_pool: null argument");
         validate_run(pool, cfg, ode, iterations, record_from);
         if (batch_capacity < 1) throw_invalid("BatchDims: batch_capacity must be >= 1");
         std::mutex mu;
-        const Run j{pool, out, cfg, ode, ev, iterations, record_from, record_mask, on_chunk, user, &mu};
+        Run j{pool, out, cfg, ode, ev, iterations, record_from, record_mask, on_chunk, user, &mu};
+        j.tally = tally;
         std::exception_ptr* failures = new std::exception_ptr[size_t(n_devices)];
         std::vector<std::thread> threads;
+        const Index N = pool->dims.problem_size;
+        const Index n_chunks = (N + batch_capacity - 1) / batch_capacity;
         for (int d = 0; d < n_devices; ++d) {
             Index b0 = 0, b1 = 0;
-            odegpu_slice(pool->dims.problem_size, n_devices, d, &b0, &b1);
+            if (chunk_aligned) { // whole chunks of batch_capacity per device, in pool order
+                Index c0 = 0, c1 = 0;
+                odegpu_slice(n_chunks, n_devices, d, &c0, &c1);
+                b0 = std::min(N, c0 * batch_capacity);
+                b1 = std::min(N, c1 * batch_capacity);
+            } else {
+                odegpu_slice(N, n_devices, d, &b0, &b1);
+            }
             const Run* jp = &j;
             std::exception_ptr* slot = failures + d;
             const int dev_id = devices[d];

@@ -27,6 +27,8 @@ scan::SolveOptions options_of(const odegpu_scan_options& o) {
     s.event_tol = o.event_tol;
     s.batch_capacity = o.batch_capacity;
     s.device = o.device;
+    if (o.n_devices > 0 && !o.devices) throw_invalid("scan: n_devices > 0 without devices");
+    for (int32_t d = 0; d < o.n_devices; ++d) s.devices.push_back(o.devices[d]);
     return s;
 }
 

@@ -41,10 +41,15 @@ class SolveOptions:  # scan.hpp:29-38
     event_tol: float = 1e-6
     batch_capacity: int = 0
     device: int = 0
+    devices: tuple = ()  # more than one: whole chunks spread over these devices
 
     def to_c(self):
+        # the device list lives on this object: the C struct is copied by value
+        self._devs = (C.c_int32 * max(len(self.devices), 1))(*self.devices)
         return abi.ScanOptions(self.algorithm, self.device, self.dt, self.rel_tol, self.abs_tol, self.event_tol,
-                               self.batch_capacity)
+                               self.batch_capacity,
+                               C.cast(self._devs, C.POINTER(C.c_int32)) if self.devices else None,
+                               len(self.devices), 0)
 
 
 @dataclass

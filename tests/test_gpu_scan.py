@@ -86,3 +86,26 @@ def test_csv_round_trip(tmp_path):
     import re
 
     assert all(re.fullmatch(r"-?\d\.\d{16}e[+-]\d{2,3}", f) for ln in lines[1:] for f in ln.split(","))
+
+
+@pytest.mark.parametrize("protocol", [abi.SCAN_DUFFING_POINCARE, abi.SCAN_VALVE, abi.SCAN_BUBBLE])
+def test_multi_device_scan_equals_single_device(protocol):
+    """Whole chunks spread over several devices (here two pipelines on device
+    0) give the one-device rows and diagnostics bit for bit."""
+    if protocol == abi.SCAN_BUBBLE:
+        mk = lambda devs: scan.BubbleScanSpec(pa1_bar=scan.ParamRange(0.5, 1.1, 5), pa2_bar=scan.ParamRange(0, 0, 1),
+                                             f1_khz=scan.ParamRange(20, 1000, 7, scan.LOG),
+                                             f2_khz=scan.ParamRange(20, 20, 1), transient=3, saved=2,
+                                             solver=scan.SolveOptions(rel_tol=1e-10, abs_tol=1e-10,
+                                                                      batch_capacity=8, devices=devs))
+    elif protocol == abi.SCAN_VALVE:
+        mk = lambda devs: scan.ValveScanSpec(q=scan.ParamRange(0.2, 10.0, 70), transient=4, saved=3,
+                                            solver=scan.SolveOptions(rel_tol=1e-10, abs_tol=1e-10,
+                                                                     batch_capacity=16, devices=devs))
+    else:
+        mk = lambda devs: scan.DuffingScanSpec(k=scan.ParamRange(0.2, 0.3, 77), transient=3, saved=2,
+                                              solver=scan.SolveOptions(batch_capacity=20, devices=devs))
+    one = scan.run(protocol, mk(()))
+    many = scan.run(protocol, mk((0, 0, 0)))
+    assert np.array_equal(one.rows.view(np.uint64), many.rows.view(np.uint64))
+    assert one.diagnostics == many.diagnostics
