@@ -34,8 +34,12 @@ template <class H, Algorithm ALG>
 void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
     constexpr int kMin = LaunchPolicy<H>::kMinBlocks;
     constexpr int kBlock = [] {
+#ifdef ODEGPU_BLOCK // tuning builds: one block size for every model
+        return ODEGPU_BLOCK;
+#else
         if constexpr (requires { LaunchPolicy<H>::kBlock; }) return LaunchPolicy<H>::kBlock;
         else return detail::kBlock;
+#endif
     }();
     auto kern = guarded_solve_kernel<H, ALG, kBlock, kMin>;
     constexpr std::size_t smem = dev::solve_smem_bytes<H, ALG, kBlock>();
