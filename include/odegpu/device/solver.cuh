@@ -808,7 +808,10 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 Real ratio = 0.0;
 #pragma unroll
                 for (int i = 0; i < N; ++i) {
-                    const Real scale = c.abs_tol[i] + c.rel_tol[i] * smax(fabs(y[i]), fabs(yn[i]));
+                    // std::max(|y|, |yn|) selected on the raw values and made
+                    // absolute in the DFMA operand (no DADDs materialising |y|)
+                    const Real big = fabs((fabs(y[i]) < fabs(yn[i])) ? yn[i] : y[i]);
+                    const Real scale = c.abs_tol[i] + c.rel_tol[i] * big;
                     ratio = smax(ratio, err[i] / scale);
                 }
                 bool accepted;

@@ -52,6 +52,38 @@ static void run_case(const char* name, const std::function<void()>& f) {
 
 constexpr Real kTwoPi = 2.0 * std::numbers::pi_v<Real>;
 
+// test_system.cpp:16-38: a deliberately broken definition (declares two
+// events, writes one) and a one-dimensional model with mutable controls.
+struct ShortEventHooks : HookDefaults {
+    static constexpr Index kSystemDim = 2, kParamCount = 0, kEventCount = 2, kAccessoryCount = 0;
+    void ode_rhs(Real, std::span<const Real>, std::span<const Real>, std::span<Real> dy) const {
+        dy[0] = 0;
+        dy[1] = 0;
+    }
+    void event_values(Real, std::span<const Real> y, std::span<const Real>, std::span<Real> f) const {
+        f[0] = y[0]; // f[1] forgotten
+    }
+};
+struct ShortEventDef : ShortEventHooks {
+    using hooks_type = ShortEventHooks;
+    SystemDims dims() const { return {2, 0, 2, 0}; }
+    OdeControls ode_controls() const { return OdeControls::uniform(2, 1e-9, 1e-9); }
+    EventControls event_controls() const {
+        return {.direction = {0, 0}, .tolerance = {1e-6, 1e-6}, .stop_condition = {0, 0}};
+    }
+};
+struct OneDimHooks : HookDefaults {
+    static constexpr Index kSystemDim = 1, kParamCount = 0, kEventCount = 0, kAccessoryCount = 0;
+    void ode_rhs(Real, std::span<const Real>, std::span<const Real>, std::span<Real> dy) const { dy[0] = 0; }
+};
+struct ControlsDef : OneDimHooks {
+    using hooks_type = OneDimHooks;
+    OdeControls ode;
+    SystemDims dims() const { return {1, 0, 0, 0}; }
+    OdeControls ode_controls() const { return ode; }
+    EventControls event_controls() const { return {}; }
+};
+
 static ProblemPool duffing_pool(Index n, Real k_lo = 0.2, Real k_hi = 0.3) { // test_batch.cpp:18-33
     ProblemPool pool(PoolDims{n, 2, 4, 0});
     for (Index i = 0; i < n; ++i) {
@@ -323,6 +355,40 @@ int main() {
         });
         CHECK(models::lyapunov_accumulate(samples[0], kTwoPi) < 0.0);
         CHECK(models::lyapunov_accumulate(samples[1], kTwoPi) > 0.0);
+    });
+
+    run_case("validate_definition (test_system.cpp:42-81)", [] {
+        models::DuffingSystem duffing;
+        const Real y0[] = {0.0, 0.0};
+        const Real p0[] = {0.2, 0.3, 1.0, 1.0};
+        validate_definition(duffing, 0.0, std::span<const Real>(y0), std::span<const Real>(p0));
+        models::ValveSystem valve;
+        const Real yv[] = {0.2, 0.0, 10.2};
+        const Real pv[] = {1.25, 10.0, 20.0, 0.3, 0.8};
+        validate_definition(valve, 0.0, std::span<const Real>(yv), std::span<const Real>(pv));
+        bool named = false;
+        try {
+            validate_definition(ShortEventDef{}, 0.0, std::span<const Real>(y0), {});
+        } catch (const std::invalid_argument& e) {
+            named = std::string(e.what()).find("event_values") != std::string::npos;
+        }
+        CHECK(named);
+        const Real y1[] = {0.0};
+        ControlsDef good;
+        good.ode = OdeControls::uniform(1, 1e-9, 1e-9);
+        validate_definition(good, 0.0, std::span<const Real>(y1), {});
+        const auto rejected = [&](auto&& mutate) {
+            ControlsDef bad;
+            bad.ode = OdeControls::uniform(1, 1e-9, 1e-9);
+            mutate(bad.ode);
+            CHECK_THROWS_AS(validate_definition(bad, 0.0, std::span<const Real>(y1), {}), std::invalid_argument);
+        };
+        rejected([](OdeControls& c) { c.min_step = 2.0 * c.max_step; });
+        rejected([](OdeControls& c) { c.abs_tol[0] = 0.0; });
+        rejected([](OdeControls& c) { c.rel_tol[0] = std::numeric_limits<Real>::quiet_NaN(); });
+        rejected([](OdeControls& c) { c.step_grow_limit = 1.0; });
+        rejected([](OdeControls& c) { c.step_shrink_limit = 1.5; });
+        rejected([](OdeControls& c) { c.rel_tol.push_back(1e-9); });
     });
 
     run_case("scan protocols: rows, order, diagnostics, CSV (scan.hpp)", [] { // test_scan.cpp:49-131
