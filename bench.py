@@ -57,7 +57,11 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2", choices=sorted(workloads.CONFIGS))
+    ap.add_argument("--config", default="cfg2", choices=sorted(workloads.CONFIGS) + ["cfg5"])
+    ap.add_argument("--log2n", type=int, default=24, help="cfg5: Keller-Miksis pool of 2^log2n systems")
+    ap.add_argument("--strong", action="store_true",
+                    help="cfg5 under torchrun: the 2^log2n pool is split over the ranks (default: each rank "
+                         "integrates 2^log2n systems)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample", type=int, default=0, help="systems in the CPU sample (0 = auto)")
@@ -72,8 +76,18 @@ def dist_env():
     return rank, world, local
 
 
-def make_workload(name: str, rank: int, world: int):
-    """Rank-local slice of the weak-scaling grid."""
+def make_workload(name: str, rank: int, world: int, args=None):
+    """Rank-local slice of the weak-scaling grid (cfg5 --strong: a contiguous
+    slice of one fixed pool, odegpu_slice's split)."""
+    if name == "cfg5":
+        wl = workloads.cfg5(args.log2n)
+        if world > 1 and args.strong:
+            lo, hi = pkg.slice_range(wl.n, world, rank)
+            wl = wl.subset(slice(lo, hi))
+            wl.description += f"; rank {rank}/{world} slice [{lo}, {hi}) (strong scaling)"
+        elif world > 1:
+            wl.description += f"; rank {rank}/{world} replica (weak scaling)"
+        return wl
     if name == "cfg2" and world > 1:
         full_k = workloads.param_range(0.2, 0.3, 1024 * world)
         wl = workloads.cfg2(1024, 1024)
@@ -177,12 +191,13 @@ def run_reference_arm(args, rank, world):
         return
     from oracle import pyoracle
 
-    wl = workloads.CONFIGS[args.config]()
+    wl = workloads.cfg5(args.log2n) if args.config == "cfg5" else workloads.CONFIGS[args.config]()
     if not pyoracle.available("reference"):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libodref.so not built"}))
         return
     cores = pyoracle.host_cores()
-    sample = args.cpu_sample or {"cfg1": 46080, "cfg2": 1 << 20, "cfg3": 1 << 17, "cfg4": 1 << 18}[args.config]
+    sample = args.cpu_sample or {"cfg1": 46080, "cfg2": 1 << 20, "cfg3": 1 << 17, "cfg4": 1 << 18,
+                                 "cfg5": 1 << 17}[args.config]
     sub = wl.strided(sample)
     # like the GPU arm, every step solves the sample from its initial
     # conditions (iterating cfg2 in place hits the reference's secant Zeno
@@ -243,7 +258,7 @@ def main():
     torch.cuda.set_device(device)
     red_dev = f"cuda:{device}" if world > 1 and torch.distributed.get_backend() == "nccl" else "cpu"
     log(f"torch ready, rank {rank}/{world} on cuda:{local}")
-    wl = make_workload(args.config, rank, world)
+    wl = make_workload(args.config, rank, world, args)
     n = wl.n
     td, y, p, acc = wl.arrays()
     pool = pkg.ProblemPool.from_arrays(td, y, p, acc)
@@ -363,7 +378,8 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        sample = args.cpu_sample or {"cfg1": 46080, "cfg2": 1 << 20, "cfg3": 1 << 18, "cfg4": 1 << 19}[args.config]
+        sample = args.cpu_sample or {"cfg1": 46080, "cfg2": 1 << 20, "cfg3": 1 << 18, "cfg4": 1 << 19,
+                                     "cfg5": 1 << 18}[args.config]
         log(f"e2e done ({e2e_value:.4e} steps/s); CPU baseline on {sample} systems")
         cpu = cpu_baseline(wl, sample)
 
@@ -380,12 +396,12 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": 1e3 * elapsed / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if (args.config == "cfg5" and args.strong) else "weak",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
         "config": {
-            "workload": wl.name,
+            "workload": wl.name if args.config != "cfg5" else f"cfg5_keller_miksis_2^{args.log2n}",
             "description": wl.description,
             "systems_per_gpu": n,
             "step": "one solve() over the batch (one forcing period for cfg1/cfg2, one collapse / section-to-"
