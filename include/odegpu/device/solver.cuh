@@ -538,24 +538,19 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
     };
     // driver.hpp:109-119: clip the next trial step onto t1; false when the
     // system is done (the lane goes to kFinish).
-    const auto setup_step = [&]() {
-        if (!(t < ODEGPU_B(t1))) {
-            phase = kFinish;
-            return;
-        }
-        Real h_try = ODEGPU_B(h);
-        clipped = false;
-        if (t + h_try >= ODEGPU_B(t1)) {
-            h_try = ODEGPU_B(t1) - t;
-            clipped = true;
-        }
-        if (!(h_try > 0)) { // fp underflow of the remaining span
-            t = ODEGPU_B(t1);
-            phase = kFinish;
-            return;
-        }
+    // Written with selects, not branches: it runs after every trial step.
+    // `live` is the loop condition t < t1 when the caller does not already
+    // know it holds (after a rejection, or an accepted step that was not
+    // clipped onto t1, it does).
+    const auto setup_step = [&](bool check_live) {
+        const Real t1 = ODEGPU_B(t1), h = ODEGPU_B(h);
+        const bool live = !check_live || t < t1;
+        clipped = t + h >= t1;
+        const Real h_try = clipped ? t1 - t : h;
+        const bool underflow = !(h_try > 0); // fp underflow of the remaining span: t = t1
+        if (live && underflow) t = t1;
         h_step = h_try;
-        phase = kReadyStep;
+        phase = (live && !underflow) ? kReadyStep : kFinish;
     };
     // EventMachine::refresh (events.hpp:160-173) from post-action values.
     const auto refresh = [&](const Real (&fp)[EE]) {
@@ -637,7 +632,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 phase = kSetup;
             }
             if (phase == kSetup) {
-                setup_step();
+                setup_step(true);
                 continue;
             }
             if (phase == kCommit) {
@@ -707,7 +702,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     phase = kFinish;
                 } else {
                     if (kAdaptive && !ODEGPU_C(relocated)) ODEGPU_B(h) = ODEGPU_C(h_next);
-                    setup_step();
+                    setup_step(true);
                 }
                 continue;
             }
@@ -836,7 +831,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 if (!accepted) { // driver.hpp:136-140; t < t1 still holds
                     ++ODEGPU_B(n_rej);
                     ODEGPU_B(h) = h_next;
-                    setup_step();
+                    setup_step(false);
                     continue;
                 }
             }
@@ -921,7 +916,9 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 continue;
             }
             ODEGPU_B(h) = h_next;
-            setup_step();
+            // landed on t1 exactly when clipped (driver.hpp:146): the loop ends
+            if (clipped) phase = kFinish;
+            else setup_step(false);
         } else if (phase == kReadySecant) { // one secant iteration's step is in (events.hpp:222-240)
             if constexpr (E > 0) {
                 Real fs[EE];
