@@ -1,5 +1,5 @@
 // solver.cuh — the sm_100a ensemble kernel: one thread integrates one system
-// at a time, entirely in registers; a lane that finishes its system fetches
+// at a time, its hot state in registers; a lane that finishes its system fetches
 // the next one from a global work counter (warp-aggregated atomics), so warps
 // stay full until the pool drains.
 //
