@@ -993,6 +993,7 @@ template <class H, Algorithm ALG, int BLOCK, int MIN_BLOCKS>
 __global__ void __launch_bounds__(BLOCK, MIN_BLOCKS)
     guarded_solve_kernel(H model, BatchArrays b, Controls c, const unsigned long long* flags) {
     if (flags[0] != ~0ull) return;
+    dmath::init_shared_tables();
     if constexpr (TrigCertifiable<H>) {
         if (flags[1] == 0) {
             solve_lanes<typename H::certified_hooks, ALG, BLOCK, EffectivePolicy<H>>(typename H::certified_hooks{},

@@ -590,7 +590,7 @@ extern "C" int odegpu_custom_end(odegpu_batch* b) {
 extern "C" int odegpu_math_check(int fn, odegpu_index n, const double* x, const double* y, double* mine,
                                  double* ref) {
     return guarded([&] {
-        if (fn < 0 || fn > 8 || n < 0 || !x || !mine || !ref || ((fn == 1 || fn == 6 || fn == 7) && !y))
+        if (fn < 0 || fn > 9 || n < 0 || !x || !mine || !ref || ((fn == 1 || fn == 6 || fn == 7) && !y))
             throw_invalid("math_check: bad arguments");
         if (n > 0) run_math_check(fn, n, x, y, mine, ref);
     });
