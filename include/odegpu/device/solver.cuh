@@ -66,9 +66,9 @@ struct BatchArrays {
     Index count;              // systems [0, count) are integrated (count <= n)
     unsigned long long* work; // next system to hand out (zeroed before launch)
     // Scan tallies (ScanDiagnostics, scan.hpp:41-49), accumulated across
-    // solves when non-null: [6] detections outside their zone, [7] max
-    // |F|/tolerance over detections (bits of a non-negative double), [8]
-    // systems whose t0 did not advance over the solve (see kTally*).
+    // solves when non-null: [5] detections, [6] detections outside their
+    // zone, [7] max |F|/tolerance over detections (bits of a non-negative
+    // double), [8] systems whose t0 did not advance over the solve (kTally*).
     unsigned long long* tally = nullptr;
 };
 
@@ -373,10 +373,10 @@ struct ColdState {
     Real f_land[E][BLOCK];
     Real prev_value[E][BLOCK]; // EventMachine (events.hpp:76-178)
     Real h_try[BLOCK], h_next[BLOCK], t_land[BLOCK];
-    Real td0_in[BLOCK];            // td[0] as fetched (scan t0-advance check)
     Real lane_max_ratio[BLOCK];    // lane accumulators for the scan tally,
     unsigned lane_outside[BLOCK];  // over every system the lane integrates
     unsigned lane_not_advanced[BLOCK];
+    unsigned lane_detections[BLOCK];
     Real th_prev[BLOCK], f_prev[BLOCK], th_cur[BLOCK], f_cur[BLOCK], th_min[BLOCK], b_th[BLOCK], b_f[BLOCK];
     long long sys[BLOCK];
     unsigned n_det[BLOCK], n_secf[BLOCK];
@@ -584,6 +584,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
     ODEGPU_C(lane_max_ratio) = 0.0;
     ODEGPU_C(lane_outside) = 0u;
     ODEGPU_C(lane_not_advanced) = 0u;
+    ODEGPU_C(lane_detections) = 0u;
 
     for (;;) {
         // ================= PREPARE: bring this lane to a pending RK evaluation
@@ -597,7 +598,6 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 if (b.reason[sys] == static_cast<std::uint8_t>(StopReason::NonFiniteAbort)) continue; // solve.hpp:98
                 ODEGPU_C(sys) = sys;
                 Real td[2] = {b.td[sys], b.td[sys + n]};
-                ODEGPU_C(td0_in) = td[0];
 #pragma unroll
                 for (int i = 0; i < N; ++i) y[i] = b.state[sys + i * n];
 #pragma unroll
@@ -665,6 +665,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                         ODEGPU_C(counter[i]) = cnt[i];
                         if (det[i]) {
                             ++ODEGPU_C(n_det);
+                            ++ODEGPU_C(lane_detections);
                             // what the scans' detection observer records
                             // (src/scan.cpp:51-61): |F|/tol and in-zone
                             const Real v = ODEGPU_C(f_land[i]);
@@ -713,6 +714,11 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 load_acc(acc);
                 m.finalize(t, S(td, 2), S(y, N), CS(prow, NP), S(acc, NA));
                 const Index sys = ODEGPU_C(sys);
+                // scan start-time check (src/scan.cpp:296-298): b.td still
+                // holds t0 as fetched
+                if (ODEGPU_C(reason) != static_cast<std::uint8_t>(StopReason::NonFiniteAbort) &&
+                    !(td[0] > b.td[sys]))
+                    ++ODEGPU_C(lane_not_advanced);
                 b.td[sys] = td[0];
                 b.td[sys + n] = td[1];
 #pragma unroll
@@ -726,9 +732,6 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 b.detections[sys] = ODEGPU_C(n_det);
                 b.secant_failures[sys] = ODEGPU_C(n_secf);
                 b.smallest_step[sys] = ODEGPU_B(smallest);
-                if (ODEGPU_C(reason) != static_cast<std::uint8_t>(StopReason::NonFiniteAbort) &&
-                    !(td[0] > ODEGPU_C(td0_in)))
-                    ++ODEGPU_C(lane_not_advanced); // scan.cpp:296-298
                 phase = kFetch;
                 continue;
             }
@@ -765,13 +768,19 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
         if (__all_sync(0xffffffffu, phase == kDone)) {
             if (b.tally) { // warp-reduced scan tally, one atomic per counter and warp
                 unsigned outside = ODEGPU_C(lane_outside), not_adv = ODEGPU_C(lane_not_advanced);
+                unsigned dets = ODEGPU_C(lane_detections);
                 Real mr = ODEGPU_C(lane_max_ratio);
                 for (int o = 16; o > 0; o >>= 1) {
                     outside += __shfl_xor_sync(0xffffffffu, outside, o);
                     not_adv += __shfl_xor_sync(0xffffffffu, not_adv, o);
+                    dets += __shfl_xor_sync(0xffffffffu, dets, o);
                     mr = smax(mr, __shfl_xor_sync(0xffffffffu, mr, o));
                 }
                 if ((threadIdx.x & 31) == 0) {
+                    // detections counted where they happen (the reference's
+                    // detection observer): a sticky-aborted system's stale
+                    // outcome record is not re-counted in later iterations
+                    if (dets) atomicAdd(b.tally + kTallyDetections, static_cast<unsigned long long>(dets));
                     if (outside) atomicAdd(b.tally + kTallyOutsideZone, static_cast<unsigned long long>(outside));
                     if (not_adv) atomicAdd(b.tally + kTallyStartNotAdvanced, static_cast<unsigned long long>(not_adv));
                     if (mr > 0) atomicMax(b.tally + kTallyMaxRatio, static_cast<unsigned long long>(__double_as_longlong(mr)));
