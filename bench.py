@@ -64,6 +64,7 @@ def parse():
                          "integrates 2^log2n systems)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-chunks", type=int, default=0, help="pipeline chunks for e2e (0 = by pool size)")
     ap.add_argument("--cpu-sample", type=int, default=0, help="systems in the CPU sample (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -347,11 +348,13 @@ def main():
         abi.OUTCOME_DTYPE)
     if world > 1:
         torch.distributed.barrier()
-    # the chunked pool pipeline: 8 chunks through a 3-stage copy-in /
-    # kernels / copy-out pipeline (odegpu_pipeline_run; 8 measured best of
-    # 4-16, scripts/e2e_chunks.py); device batches and pinned staging are
-    # allocated once, like a scan driver would
-    cap = max(1, n // 8)
+    # the chunked pool pipeline: chunks through a 3-stage copy-in / kernels /
+    # copy-out pipeline (odegpu_pipeline_run); device batches and pinned
+    # staging are allocated once, like a scan driver would. Chunk count
+    # (scripts/e2e_chunks.py): ~64 Ki systems per chunk, 2..8 chunks for the
+    # transfer-bound cheap models, up to 16 for Keller-Miksis
+    n_chunks = args.e2e_chunks or int(min(max(round(n / 65536), 2), 16 if wl.instr_per_step > 500 else 8))
+    cap = max(1, -(-n // n_chunks))
     pipe = pkg.api.Pipeline(wl.model, cap, device)
     outs = (o_td, o_y, o_a, outc)
     pipe.run(pin_pool, cfg, 1, out_arrays=outs)  # warm-up (first-touch of the output pages)
@@ -433,7 +436,7 @@ def main():
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "steps": args.e2e_steps,
-                "path": "odegpu_pipeline_run over the pinned host pool: 8 chunks, H2D / kernels / D2H of td, "
+                "path": f"odegpu_pipeline_run over the pinned host pool: {n_chunks} chunks, H2D / kernels / D2H of td, "
                         "state, accessories and outcome records on separate streams (4 chunks in flight), "
                         "into host arrays, wall-clock"},
         "cpu_baseline": cpu,

@@ -1,10 +1,11 @@
-"""e2e (host buffers through odegpu_pipeline_run) vs chunk count, cfg2 full size."""
+"""e2e (host buffers through odegpu_pipeline_run) vs chunk count: python scripts/e2e_chunks.py [cfg] [chunks...]"""
 import sys, time
 sys.path.insert(0, ".")
 import numpy as np, torch
 import paper_1810_03931_b200 as pkg
 from paper_1810_03931_b200 import abi, workloads
-wl = workloads.cfg2()
+cfg = sys.argv[1] if len(sys.argv) > 1 else 'cfg2'
+wl = workloads.CONFIGS[cfg]()
 n = wl.n
 td, y, p, acc = wl.arrays()
 pin = lambda a: torch.from_numpy(a).pin_memory().numpy()
@@ -13,7 +14,7 @@ pool._td, pool._state, pool._params, pool._acc = pin(td), pin(y), pin(p), pin(ac
 outs = (pin(np.zeros(2 * n)), pin(np.zeros(y.size)), pin(np.zeros(acc.size)),
         torch.zeros(n * abi.OUTCOME_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True).numpy().view(abi.OUTCOME_DTYPE))
 cfg = pkg.SolverConfig(wl.algorithm, wl.dt)
-for chunks in (4, 8, 12, 16):
+for chunks in [int(a) for a in sys.argv[2:]] or (4, 8, 12, 16):
     pipe = pkg.api.Pipeline(wl.model, n // chunks, 0)
     pipe.run(pool, cfg, 1, out_arrays=outs)
     best = 1e9
