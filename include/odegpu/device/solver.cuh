@@ -118,11 +118,39 @@ __device__ __forceinline__ Real sclamp(Real v, Real lo, Real hi) { return (v < l
 /// register file across the RK stages).
 __device__ __forceinline__ void cold_fence() { asm volatile("" ::: "memory"); }
 
+/// A state vector passed by value (registers) through an outlined RHS call.
+template <int N>
+struct StateVec {
+    Real v[N];
+};
+
+/// The model's RHS as a real (non-inlined) device function: its register
+/// allocation is its own, not interleaved with the step loop's. For a large
+/// RHS (Keller-Miksis) this is what lets straight-line stages stay small in
+/// code and in registers.
 template <class H>
+__device__ __noinline__ StateVec<H::kSystemDim> rhs_outline(const H m, Real t, StateVec<H::kSystemDim> y,
+                                                            const Real* p) {
+    StateVec<H::kSystemDim> dy;
+    m.ode_rhs(t, std::span<const Real>(y.v, H::kSystemDim), std::span<const Real>(p, H::kParamCount),
+              std::span<Real>(dy.v, H::kSystemDim));
+    return dy;
+}
+
+template <class H, bool OUTLINE = false>
 __device__ __forceinline__ void rhs(const H& m, Real t, const Real (&y)[H::kSystemDim],
                                     const Real* p, Real (&dy)[H::kSystemDim]) {
-    m.ode_rhs(t, std::span<const Real>(y, H::kSystemDim), std::span<const Real>(p, H::kParamCount),
-              std::span<Real>(dy, H::kSystemDim));
+    if constexpr (OUTLINE) {
+        StateVec<H::kSystemDim> in;
+#pragma unroll
+        for (int i = 0; i < H::kSystemDim; ++i) in.v[i] = y[i];
+        const StateVec<H::kSystemDim> out = rhs_outline<H>(m, t, in, p);
+#pragma unroll
+        for (int i = 0; i < H::kSystemDim; ++i) dy[i] = out.v[i];
+    } else {
+        m.ode_rhs(t, std::span<const Real>(y, H::kSystemDim), std::span<const Real>(p, H::kParamCount),
+                  std::span<Real>(dy, H::kSystemDim));
+    }
 }
 
 /// One trial step from (t, y) with step h (steppers.hpp:82-139). Writes the
@@ -139,7 +167,7 @@ __device__ __forceinline__ void rhs(const H& m, Real t, const Real (&y)[H::kSyst
 /// (kb: this thread's column, stride BLOCK — conflict-free): a loop-carried
 /// k1..k5 in registers costs ~20 registers across the RHS plus register
 /// moves at every stage, while the smem form costs ~40 LDS/STS per step.
-template <class H, Algorithm ALG, bool ROLLED, int BLOCK>
+template <class H, Algorithm ALG, bool ROLLED, int BLOCK, bool OUTLINE = false>
 __device__ __forceinline__ bool rk_step(const H& m, Real t, Real h, const Real (&y)[H::kSystemDim],
                                         const Real* p, Real (&out)[H::kSystemDim],
                                         Real (&err)[H::kSystemDim], Real* kb) {
@@ -151,16 +179,16 @@ __device__ __forceinline__ bool rk_step(const H& m, Real t, Real h, const Real (
         Real k1[N], k2[N], k3[N], k4[N], k5[N], k6[N];
         Real yt[N];
         if constexpr (ALG == Algorithm::RK4) {
-            rhs(m, t, y, p, k1);
+            rhs<H, OUTLINE>(m, t, y, p, k1);
 #pragma unroll
             for (int i = 0; i < N; ++i) yt[i] = y[i] + 0.5 * h * k1[i];
-            rhs(m, t + 0.5 * h, yt, p, k2);
+            rhs<H, OUTLINE>(m, t + 0.5 * h, yt, p, k2);
 #pragma unroll
             for (int i = 0; i < N; ++i) yt[i] = y[i] + 0.5 * h * k2[i];
-            rhs(m, t + 0.5 * h, yt, p, k3);
+            rhs<H, OUTLINE>(m, t + 0.5 * h, yt, p, k3);
 #pragma unroll
             for (int i = 0; i < N; ++i) yt[i] = y[i] + h * k3[i];
-            rhs(m, t + h, yt, p, k4);
+            rhs<H, OUTLINE>(m, t + h, yt, p, k4);
 #pragma unroll
             for (int i = 0; i < N; ++i) {
                 out[i] = y[i] + (h / 6.0) * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
@@ -168,25 +196,25 @@ __device__ __forceinline__ bool rk_step(const H& m, Real t, Real h, const Real (
                 finite = finite && isfinite(out[i]);
             }
         } else {
-            rhs(m, t, y, p, k1);
+            rhs<H, OUTLINE>(m, t, y, p, k1);
 #pragma unroll
             for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a21 * k1[i]);
-            rhs(m, t + ck::c2 * h, yt, p, k2);
+            rhs<H, OUTLINE>(m, t + ck::c2 * h, yt, p, k2);
 #pragma unroll
             for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a31 * k1[i] + ck::a32 * k2[i]);
-            rhs(m, t + ck::c3 * h, yt, p, k3);
+            rhs<H, OUTLINE>(m, t + ck::c3 * h, yt, p, k3);
 #pragma unroll
             for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a41 * k1[i] + ck::a42 * k2[i] + ck::a43 * k3[i]);
-            rhs(m, t + ck::c4 * h, yt, p, k4);
+            rhs<H, OUTLINE>(m, t + ck::c4 * h, yt, p, k4);
 #pragma unroll
             for (int i = 0; i < N; ++i)
                 yt[i] = y[i] + h * (ck::a51 * k1[i] + ck::a52 * k2[i] + ck::a53 * k3[i] + ck::a54 * k4[i]);
-            rhs(m, t + ck::c5 * h, yt, p, k5);
+            rhs<H, OUTLINE>(m, t + ck::c5 * h, yt, p, k5);
 #pragma unroll
             for (int i = 0; i < N; ++i)
                 yt[i] = y[i] + h * (ck::a61 * k1[i] + ck::a62 * k2[i] + ck::a63 * k3[i] + ck::a64 * k4[i] +
                                     ck::a65 * k5[i]);
-            rhs(m, t + ck::c6 * h, yt, p, k6);
+            rhs<H, OUTLINE>(m, t + ck::c6 * h, yt, p, k6);
 #pragma unroll
             for (int i = 0; i < N; ++i) {
                 out[i] = y[i] + h * (ck::b1 * k1[i] + ck::b3 * k3[i] + ck::b4 * k4[i] + ck::b6 * k6[i]);
@@ -227,7 +255,7 @@ __device__ __forceinline__ bool rk_step(const H& m, Real t, Real h, const Real (
                 for (int i = 0; i < N; ++i) yt[i] = y[i] + h * ODEGPU_K(3, i);
                 break;
             }
-            rhs(m, ts, yt, p, kk);
+            rhs<H, OUTLINE>(m, ts, yt, p, kk);
             if (s < 4) {
 #pragma unroll
                 for (int i = 0; i < N; ++i) ODEGPU_K(s, i) = kk[i];
@@ -283,7 +311,7 @@ __device__ __forceinline__ bool rk_step(const H& m, Real t, Real h, const Real (
                                         ck::a65 * ODEGPU_K(5, i));
                 break;
             }
-            rhs(m, ts, yt, p, kk);
+            rhs<H, OUTLINE>(m, ts, yt, p, kk);
             if (s < 6) {
 #pragma unroll
                 for (int i = 0; i < N; ++i) ODEGPU_K(s, i) = kk[i];
@@ -413,7 +441,10 @@ inline constexpr bool kHasOrdinaryAccessory = !std::is_same_v<decltype(&H::ordin
 ///                      odd stride per thread, conflict-free 8-byte loads);
 ///  * kBookInShared   — the per-step bookkeeping (Bookkeeping) in shared
 ///                      memory: a few LDS/STS per step for fewer registers
-///                      across the stages (large RHS, high register demand).
+///                      across the stages (large RHS, high register demand);
+///  * kOutlineRhs     — the RHS as a real call (rhs_outline) instead of
+///                      inlined into each stage: a large RHS keeps its own
+///                      register allocation and is emitted once.
 /// ODEGPU_POLICY_{ROLLED,COLD_SHARED,PARAMS_SHARED} override every model in
 /// tuning builds (scripts/build_variants.sh).
 template <class H>
@@ -422,6 +453,7 @@ struct KernelPolicy {
     static constexpr bool kColdInShared = true;
     static constexpr bool kParamsInShared = false;
     static constexpr bool kBookInShared = false;
+    static constexpr bool kOutlineRhs = false;
 };
 
 template <class H>
@@ -440,6 +472,14 @@ struct EffectivePolicy {
     static constexpr bool kParamsInShared = ODEGPU_POLICY_PARAMS_SHARED && H::kParamCount > 0;
 #else
     static constexpr bool kParamsInShared = KernelPolicy<H>::kParamsInShared && H::kParamCount > 0;
+#endif
+#ifdef ODEGPU_POLICY_OUTLINE_RHS
+    static constexpr bool kOutlineRhs = ODEGPU_POLICY_OUTLINE_RHS;
+#else
+    static constexpr bool kOutlineRhs = [] {
+        if constexpr (requires { KernelPolicy<H>::kOutlineRhs; }) return KernelPolicy<H>::kOutlineRhs;
+        else return false;
+    }();
 #endif
 #ifdef ODEGPU_POLICY_BOOK_SHARED
     static constexpr bool kBookInShared = ODEGPU_POLICY_BOOK_SHARED;
@@ -792,7 +832,8 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
         // ================= the shared Runge-Kutta evaluation
         if constexpr (kFence) cold_fence();
         Real yn[N], err[N];
-        const bool nonfinite = rk_step<H, ALG, Pol::kRolledStages, BLOCK>(m, t, h_step, y, prow, yn, err, kbuf);
+        const bool nonfinite =
+            rk_step<H, ALG, Pol::kRolledStages, BLOCK, Pol::kOutlineRhs>(m, t, h_step, y, prow, yn, err, kbuf);
         if constexpr (kFence) cold_fence();
 
         // ================= ABSORB

@@ -3,6 +3,23 @@
 #include "launch.cuh"
 #include "test_fakes.cuh"
 
+// Two of the fakes run the kernel structures no built-in model uses any
+// more, so the golden tests keep them covered: the rolled stage loop with
+// shared-memory stage vectors (SeatContact: 3 states, 2 events, impact) and
+// the outlined RHS with the bookkeeping in shared memory (Ramp: secant,
+// stops, direction filter).
+namespace odegpu::device {
+template <>
+struct KernelPolicy<fakes::SeatContactHooks> {
+    static constexpr bool kRolledStages = true, kColdInShared = true, kParamsInShared = true, kBookInShared = true;
+};
+template <>
+struct KernelPolicy<fakes::RampHooks> {
+    static constexpr bool kRolledStages = false, kColdInShared = true, kParamsInShared = false, kBookInShared = true,
+                          kOutlineRhs = true;
+};
+} // namespace odegpu::device
+
 namespace odegpu::detail {
 
 bool family_dims_fakes(const odegpu_model& m, odegpu_system_dims* d) {

@@ -3,34 +3,35 @@
 #include "launch.cuh"
 #include "odegpu/models/keller_miksis.hpp"
 
+// Keller-Miksis: the RHS (pow + 2 sincos + 4 quotients) is large. It is an
+// outlined call (one copy of its code, its own register allocation), so the
+// six stages can be straight-line with k1..k6 in registers — no stage switch,
+// no shared-memory stage vectors: 96 registers instead of the 128 the inlined
+// rolled loop needed. With the bookkeeping in registers and the cold state +
+// 13 coefficients in shared memory (40 KB per block) 5 blocks of 128 fit per
+// SM: 15.5 -> 14.4 ms on cfg3 (rolled/inlined, 4 blocks) — DESIGN.md §3.1.
 namespace odegpu::device {
 template <>
 struct KernelPolicy<odegpu::models::BubbleCollapseHooks> {
-    static constexpr bool kRolledStages = true, kColdInShared = true, kParamsInShared = true, kBookInShared = true;
+    static constexpr bool kRolledStages = false, kColdInShared = true, kParamsInShared = true, kBookInShared = false,
+                          kOutlineRhs = true;
 };
-} // namespace odegpu::device
-
-namespace odegpu::device {
 template <>
 struct KernelPolicy<odegpu::models::KellerMiksisHooks> {
-    static constexpr bool kRolledStages = true, kColdInShared = true, kParamsInShared = true, kBookInShared = true;
+    static constexpr bool kRolledStages = false, kColdInShared = true, kParamsInShared = true, kBookInShared = false,
+                          kOutlineRhs = true;
 };
 } // namespace odegpu::device
 
 namespace odegpu::detail {
 
-// Keller-Miksis: the RHS (pow + 2 sincos + 4 divisions) is large, so the six
-// stages share one RHS call site (rolled loop: I-cache) and both the cold
-// state and the 13 coefficients live in shared memory (profiles/r01_variants.md:
-// 22.98 ms vs 24.1 ms unrolled). 4 blocks/SM: at 5 ptxas spills 84 B, and the
-// stage vectors must stay in registers.
 template <>
 struct LaunchPolicy<models::BubbleCollapseHooks> {
-    static constexpr int kMinBlocks = ODEGPU_MB(4);
+    static constexpr int kMinBlocks = ODEGPU_MB(5);
 };
 template <>
 struct LaunchPolicy<models::KellerMiksisHooks> {
-    static constexpr int kMinBlocks = ODEGPU_MB(4);
+    static constexpr int kMinBlocks = ODEGPU_MB(5);
 };
 
 bool family_dims_keller_miksis(const odegpu_model& m, odegpu_system_dims* d) {
