@@ -153,6 +153,67 @@ __device__ __forceinline__ void rhs(const H& m, Real t, const Real (&y)[H::kSyst
     }
 }
 
+/// Number of cached time terms of a model (hooks.hpp TimeSplitHooks), 0 if
+/// it does not split its RHS.
+template <class H>
+inline constexpr int kTimeTerms = [] {
+    if constexpr (TimeSplitHooks<H>) return static_cast<int>(H::kTimeTermCount);
+    else return 0;
+}();
+
+/// The outlined halves of a time-split model's RHS: its time terms, and the
+/// RHS given them.
+template <class H>
+__device__ __noinline__ StateVec<kTimeTerms<H>> time_terms_outline(const H m, Real t, const Real* p) {
+    StateVec<kTimeTerms<H>> tt;
+    m.time_terms(t, std::span<const Real>(p, H::kParamCount), std::span<Real>(tt.v, kTimeTerms<H>));
+    return tt;
+}
+template <class H>
+__device__ __noinline__ StateVec<H::kSystemDim> rhs_split_outline(const H m, Real t, StateVec<H::kSystemDim> y,
+                                                                  const Real* p, StateVec<kTimeTerms<H>> tt) {
+    StateVec<H::kSystemDim> dy;
+    m.ode_rhs_split(t, std::span<const Real>(y.v, H::kSystemDim), std::span<const Real>(p, H::kParamCount),
+                    std::span<const Real>(tt.v, kTimeTerms<H>), std::span<Real>(dy.v, H::kSystemDim));
+    return dy;
+}
+
+/// One RHS evaluation of a time-split model at stage time t: the time terms
+/// tt are computed when `need` (and returned in tt), reused otherwise.
+template <class H, bool OUTLINE>
+__device__ __forceinline__ void rhs_tt(const H& m, Real t, const Real (&y)[H::kSystemDim], const Real* p,
+                                       Real (&tt)[kTimeTerms<H>], bool need, Real (&dy)[H::kSystemDim]) {
+    constexpr int N = H::kSystemDim, K = kTimeTerms<H>;
+    if constexpr (OUTLINE) {
+        StateVec<K> tin;
+        if (need) {
+            tin = time_terms_outline<H>(m, t, p);
+        } else {
+#pragma unroll
+            for (int i = 0; i < K; ++i) tin.v[i] = tt[i];
+        }
+        StateVec<N> in;
+#pragma unroll
+        for (int i = 0; i < N; ++i) in.v[i] = y[i];
+        const StateVec<N> out = rhs_split_outline<H>(m, t, in, p, tin);
+#pragma unroll
+        for (int i = 0; i < N; ++i) dy[i] = out.v[i];
+#pragma unroll
+        for (int i = 0; i < K; ++i) tt[i] = tin.v[i];
+    } else {
+        if (need) m.time_terms(t, std::span<const Real>(p, H::kParamCount), std::span<Real>(tt, K));
+        m.ode_rhs_split(t, std::span<const Real>(y, N), std::span<const Real>(p, H::kParamCount),
+                        std::span<const Real>(tt, K), std::span<Real>(dy, N));
+    }
+}
+
+/// A stage evaluation that does not touch the time-term cache.
+template <class H, bool OUTLINE>
+__device__ __forceinline__ void rhs_stage(const H& m, Real t, const Real (&y)[H::kSystemDim], const Real* p,
+                                          Real (&dy)[H::kSystemDim]) {
+    rhs<H, OUTLINE>(m, t, y, p, dy);
+}
+
 /// One trial step from (t, y) with step h (steppers.hpp:82-139). Writes the
 /// proposed state, the embedded error |y5 - y4| (RKCK45) and whether
 /// anything is non-finite. Expressions are those of the reference, operation
@@ -167,28 +228,55 @@ __device__ __forceinline__ void rhs(const H& m, Real t, const Real (&y)[H::kSyst
 /// (kb: this thread's column, stride BLOCK — conflict-free): a loop-carried
 /// k1..k5 in registers costs ~20 registers across the RHS plus register
 /// moves at every stage, while the smem form costs ~40 LDS/STS per step.
-template <class H, Algorithm ALG, bool ROLLED, int BLOCK, bool OUTLINE = false>
+///
+/// Time-split models (kTimeTerms<H> > 0, straight-line stages) go through
+/// the lane's time-term cache `tc` (TimeTermCache): the first stage reuses
+/// the terms at t if either slot holds them, and the step leaves the terms
+/// at t (slot 0: a rejected step's retry, a secant re-step) and at t + h
+/// (slot 1: the next step when this one is accepted) behind.
+template <class H, Algorithm ALG, bool ROLLED, int BLOCK, bool OUTLINE, class TC>
 __device__ __forceinline__ bool rk_step(const H& m, Real t, Real h, const Real (&y)[H::kSystemDim],
                                         const Real* p, Real (&out)[H::kSystemDim],
-                                        Real (&err)[H::kSystemDim], Real* kb) {
+                                        Real (&err)[H::kSystemDim], Real* kb, const TC& tc) {
     constexpr int N = H::kSystemDim;
+    constexpr int K = kTimeTerms<H>;
     bool finite = true;
+    // the first stage and the stage at t + h through the time-term cache
+    const auto first = [&](Real (&dy)[N]) {
+        if constexpr (TC::kEnabled && K > 0 && !ROLLED) {
+            Real tt[K];
+            const bool hit = tc.lookup(t, tt);
+            rhs_tt<H, OUTLINE>(m, t, y, p, tt, !hit, dy);
+            tc.store(0, t, tt);
+        } else {
+            rhs_stage<H, OUTLINE>(m, t, y, p, dy);
+        }
+    };
+    const auto at_end = [&](const Real (&ys)[N], Real (&dy)[N]) {
+        if constexpr (TC::kEnabled && K > 0 && !ROLLED) {
+            Real tt[K];
+            rhs_tt<H, OUTLINE>(m, t + h, ys, p, tt, true, dy);
+            tc.store(1, t + h, tt);
+        } else {
+            rhs_stage<H, OUTLINE>(m, t + h, ys, p, dy);
+        }
+    };
     if constexpr (!ROLLED) {
         // Straight-line stages: best when the RHS is small (Duffing, valve):
         // no stage dispatch, the scheduler sees across stage boundaries.
         Real k1[N], k2[N], k3[N], k4[N], k5[N], k6[N];
         Real yt[N];
         if constexpr (ALG == Algorithm::RK4) {
-            rhs<H, OUTLINE>(m, t, y, p, k1);
+            first(k1);
 #pragma unroll
             for (int i = 0; i < N; ++i) yt[i] = y[i] + 0.5 * h * k1[i];
-            rhs<H, OUTLINE>(m, t + 0.5 * h, yt, p, k2);
+            rhs_stage<H, OUTLINE>(m, t + 0.5 * h, yt, p, k2);
 #pragma unroll
             for (int i = 0; i < N; ++i) yt[i] = y[i] + 0.5 * h * k2[i];
-            rhs<H, OUTLINE>(m, t + 0.5 * h, yt, p, k3);
+            rhs_stage<H, OUTLINE>(m, t + 0.5 * h, yt, p, k3);
 #pragma unroll
             for (int i = 0; i < N; ++i) yt[i] = y[i] + h * k3[i];
-            rhs<H, OUTLINE>(m, t + h, yt, p, k4);
+            at_end(yt, k4);
 #pragma unroll
             for (int i = 0; i < N; ++i) {
                 out[i] = y[i] + (h / 6.0) * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
@@ -196,25 +284,26 @@ __device__ __forceinline__ bool rk_step(const H& m, Real t, Real h, const Real (
                 finite = finite && isfinite(out[i]);
             }
         } else {
-            rhs<H, OUTLINE>(m, t, y, p, k1);
+            first(k1);
 #pragma unroll
             for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a21 * k1[i]);
-            rhs<H, OUTLINE>(m, t + ck::c2 * h, yt, p, k2);
+            rhs_stage<H, OUTLINE>(m, t + ck::c2 * h, yt, p, k2);
 #pragma unroll
             for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a31 * k1[i] + ck::a32 * k2[i]);
-            rhs<H, OUTLINE>(m, t + ck::c3 * h, yt, p, k3);
+            rhs_stage<H, OUTLINE>(m, t + ck::c3 * h, yt, p, k3);
 #pragma unroll
             for (int i = 0; i < N; ++i) yt[i] = y[i] + h * (ck::a41 * k1[i] + ck::a42 * k2[i] + ck::a43 * k3[i]);
-            rhs<H, OUTLINE>(m, t + ck::c4 * h, yt, p, k4);
+            rhs_stage<H, OUTLINE>(m, t + ck::c4 * h, yt, p, k4);
 #pragma unroll
             for (int i = 0; i < N; ++i)
                 yt[i] = y[i] + h * (ck::a51 * k1[i] + ck::a52 * k2[i] + ck::a53 * k3[i] + ck::a54 * k4[i]);
-            rhs<H, OUTLINE>(m, t + ck::c5 * h, yt, p, k5);
+            static_assert(ck::c5 == 1.0, "Cash-Karp stage 5 is the step's end point");
+            at_end(yt, k5);
 #pragma unroll
             for (int i = 0; i < N; ++i)
                 yt[i] = y[i] + h * (ck::a61 * k1[i] + ck::a62 * k2[i] + ck::a63 * k3[i] + ck::a64 * k4[i] +
                                     ck::a65 * k5[i]);
-            rhs<H, OUTLINE>(m, t + ck::c6 * h, yt, p, k6);
+            rhs_stage<H, OUTLINE>(m, t + ck::c6 * h, yt, p, k6);
 #pragma unroll
             for (int i = 0; i < N; ++i) {
                 out[i] = y[i] + h * (ck::b1 * k1[i] + ck::b3 * k3[i] + ck::b4 * k4[i] + ck::b6 * k6[i]);
@@ -390,7 +479,7 @@ constexpr int kMaxSecantIterations = 50; // events.hpp:190
 /// memory as structure of arrays (one column per thread, bank-conflict free)
 /// so that only the hot set — t, h, y, the step bookkeeping and the stage
 /// vectors — occupies registers; that is what sets occupancy.
-template <class H, int BLOCK>
+template <class H, int BLOCK, bool TT = false>
 struct ColdState {
     static constexpr int N = H::kSystemDim;
     static constexpr int E = H::kEventCount > 0 ? H::kEventCount : 1;
@@ -411,6 +500,33 @@ struct ColdState {
     int counter[E][BLOCK];
     int s_it[BLOCK], s_idx[BLOCK], located[BLOCK];
     unsigned char clipped[BLOCK], relocated[BLOCK], s_conv[BLOCK], reason[BLOCK];
+    // time-term cache of a time-split model (rk_step): slot s holds the
+    // terms at tt_key[s]
+    static constexpr int TTB = TT ? BLOCK : 1;
+    Real tt_key[2][TTB];
+    Real tt_val[2][kTimeTerms<H> > 0 ? kTimeTerms<H> : 1][TTB];
+};
+
+/// A lane's view of its time-term cache (two slots in its ColdState column).
+template <class CS, int K, bool ENABLED>
+struct TimeTermCache {
+    static constexpr bool kEnabled = ENABLED;
+    CS& cs;
+    int tid;
+    __device__ __forceinline__ bool lookup(Real t, Real (&tt)[K]) const {
+        const bool in1 = t == cs.tt_key[1][tid];
+#pragma unroll
+        for (int i = 0; i < K; ++i) tt[i] = in1 ? cs.tt_val[1][i][tid] : cs.tt_val[0][i][tid];
+        return in1 || t == cs.tt_key[0][tid];
+    }
+    __device__ __forceinline__ void store(int slot, Real key, const Real (&tt)[K]) const {
+        cs.tt_key[slot][tid] = key;
+#pragma unroll
+        for (int i = 0; i < K; ++i) cs.tt_val[slot][i][tid] = tt[i];
+    }
+    __device__ __forceinline__ void clear() const {
+        cs.tt_key[0][tid] = cs.tt_key[1][tid] = __longlong_as_double(0x7ff8000000000000LL); // NaN
+    }
 };
 
 /// Per-step bookkeeping of a lane (t1, SystemOutcome counters, EventMachine
@@ -454,6 +570,7 @@ struct KernelPolicy {
     static constexpr bool kParamsInShared = false;
     static constexpr bool kBookInShared = false;
     static constexpr bool kOutlineRhs = false;
+    static constexpr bool kCacheTimeTerms = true;
 };
 
 template <class H>
@@ -489,6 +606,17 @@ struct EffectivePolicy {
         else return false; // specialisations written before the flag existed
     }();
 #endif
+    // the time-term cache (rk_step, TimeTermCache): time-split models with
+    // straight-line stages, unless the policy declines it
+    static constexpr bool kCacheTimeTerms = [] {
+#ifdef ODEGPU_POLICY_CACHE_TT
+        if constexpr (true) return ODEGPU_POLICY_CACHE_TT && kTimeTerms<H> > 0 && !kRolledStages;
+        else
+#endif
+        if constexpr (requires { KernelPolicy<H>::kCacheTimeTerms; })
+            return KernelPolicy<H>::kCacheTimeTerms && kTimeTerms<H> > 0 && !kRolledStages;
+        else return kTimeTerms<H> > 0 && !kRolledStages;
+    }();
     static constexpr int kParamStride = kParamsInShared ? (H::kParamCount | 1) : 1;
     static constexpr int kParamRegs = kParamsInShared ? 1 : (H::kParamCount > 0 ? H::kParamCount : 1);
 };
@@ -497,7 +625,7 @@ struct EffectivePolicy {
 /// memory: the Keller-Miksis layout exceeds the 48 KB static limit).
 template <class H, Algorithm ALG, int BLOCK, class Pol = EffectivePolicy<H>>
 struct SharedLayout {
-    ColdState<H, Pol::kColdInShared ? BLOCK : 1> cold;
+    ColdState<H, Pol::kColdInShared ? BLOCK : 1, Pol::kCacheTimeTerms> cold;
     Bookkeeping<Pol::kBookInShared ? BLOCK : 1> book;
     Real params[Pol::kParamsInShared ? BLOCK * Pol::kParamStride : 1];
     Real k[Pol::kRolledStages ? (ALG == Algorithm::RK4 ? 3 : 5) * H::kSystemDim * BLOCK : 1];
@@ -529,16 +657,20 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
     constexpr bool kAdaptive = ALG == Algorithm::RKCK45;
     static_assert(N <= kMaxDim && E <= kMaxEvents, "model wider than the device controls");
     constexpr bool kFence = Pol::kColdInShared || Pol::kParamsInShared || Pol::kBookInShared;
+    constexpr bool kCacheTT = Pol::kCacheTimeTerms;
 
     // cold state: a shared-memory column per thread, or a register record
     extern __shared__ __align__(16) unsigned char odegpu_dsmem[];
     auto& sh = *reinterpret_cast<SharedLayout<H, ALG, BLOCK, Pol>*>(odegpu_dsmem);
-    ColdState<H, 1> cs_regs;
+    ColdState<H, 1, Pol::kCacheTimeTerms> cs_regs;
     auto& cs = *[&] {
         if constexpr (Pol::kColdInShared) return &sh.cold;
         else return &cs_regs;
     }();
     const int tid = Pol::kColdInShared ? static_cast<int>(threadIdx.x) : 0;
+    const TimeTermCache<std::remove_reference_t<decltype(cs)>, (kTimeTerms<H> > 0 ? kTimeTerms<H> : 1), kCacheTT> ttc{
+        cs, tid};
+    if constexpr (kCacheTT) ttc.clear();
     Real* const sp = sh.params;
     // stage derivatives of the rolled stage loop (rk_step)
     Real* const kbuf = sh.k + (Pol::kRolledStages ? threadIdx.x : 0);
@@ -637,6 +769,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 }
                 if (b.reason[sys] == static_cast<std::uint8_t>(StopReason::NonFiniteAbort)) continue; // solve.hpp:98
                 ODEGPU_C(sys) = sys;
+                if constexpr (kCacheTT) ttc.clear(); // new parameters
                 Real td[2] = {b.td[sys], b.td[sys + n]};
 #pragma unroll
                 for (int i = 0; i < N; ++i) y[i] = b.state[sys + i * n];
@@ -833,7 +966,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
         if constexpr (kFence) cold_fence();
         Real yn[N], err[N];
         const bool nonfinite =
-            rk_step<H, ALG, Pol::kRolledStages, BLOCK, Pol::kOutlineRhs>(m, t, h_step, y, prow, yn, err, kbuf);
+            rk_step<H, ALG, Pol::kRolledStages, BLOCK, Pol::kOutlineRhs>(m, t, h_step, y, prow, yn, err, kbuf, ttc);
         if constexpr (kFence) cold_fence();
 
         // ================= ABSORB

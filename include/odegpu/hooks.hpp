@@ -60,6 +60,24 @@ concept DeviceHooks = std::is_trivially_copyable_v<H> &&
     { d.initialize(t, td, my, p, acc) } -> std::same_as<void>;
     { d.finalize(t, td, my, p, acc) } -> std::same_as<void>;
 };
+
+/// Optional split of ode_rhs (an extension, not a reference hook): the terms
+/// that depend on t and the parameters only — the excitation, cos(omega t)
+/// or the driving phases' sines — and the rest. A model declaring it
+/// guarantees, bit for bit,
+///   ode_rhs(t, y, p, dy)  ==  { time_terms(t, p, tt); ode_rhs_split(t, y, p, tt, dy); }
+/// and the solver then evaluates the time terms once per distinct stage
+/// time: an accepted step's end point (stage t + h: RK4 stage 4, Cash-Karp
+/// stage 5) is the next step's first stage, and a rejected step's retry
+/// starts from the same t (device/solver.cuh, TimeTermCache).
+template <typename H>
+concept TimeSplitHooks = DeviceHooks<H> &&
+    requires(const H& d, Real t, std::span<const Real> y, std::span<const Real> p, std::span<const Real> tt,
+             std::span<Real> out) {
+    { H::kTimeTermCount } -> std::convertible_to<Index>;
+    { d.time_terms(t, p, out) } -> std::same_as<void>;
+    { d.ode_rhs_split(t, y, p, tt, out) } -> std::same_as<void>;
+} && (H::kTimeTermCount > 0);
 // clang-format on
 
 } // namespace odegpu

@@ -44,6 +44,17 @@ struct DuffingHooksT : HookDefaults {
     ODEGPU_HD void ode_rhs(Real t, std::span<const Real> y, std::span<const Real> p, std::span<Real> dy) const {
         duffing_rhs<T>(t, y, p, dy);
     }
+    // time split (hooks.hpp TimeSplitHooks): the forcing cos(omega t)
+    static constexpr Index kTimeTermCount = 1;
+    ODEGPU_HD void time_terms(Real t, std::span<const Real> p, std::span<Real> tt) const {
+        tt[0] = T::cos(p[3] * t);
+    }
+    ODEGPU_HD void ode_rhs_split(Real, std::span<const Real> y, std::span<const Real> p, std::span<const Real> tt,
+                                 std::span<Real> dy) const {
+        const Real k = p[0], B = p[1], delta = p[2];
+        dy[0] = y[1];
+        dy[1] = delta * y[0] - y[0] * y[0] * y[0] - k * y[1] + B * tt[0];
+    }
     ODEGPU_HD static Real trig_argument_bound(Real t0, Real t1, const Real* p, Index stride) {
         return fabs(p[3 * stride]) * fmax(fabs(t0), fabs(t1));
     }

@@ -17,25 +17,35 @@
 
 namespace odegpu::models {
 
-/// Dimensionless Keller-Miksis RHS (keller_miksis.hpp:82-103), same
-/// operation order. y1 <= 0 yields NaN derivatives for the step control.
-/// On the device sin/cos of the same argument share one range reduction
-/// (sincos), as the reference's g++ build merges them into glibc sincos.
+/// The excitation terms of the Keller-Miksis RHS, which depend on tau and
+/// the coefficients only: tt = [c5 sin(2 pi tau) + c6 sin(arg2),
+/// c7 cos(2 pi tau) + c8 cos(arg2)], arg2 = 2 pi c11 tau + c12
+/// (keller_miksis.hpp:93-99). On the device sin/cos of the same argument
+/// share one range reduction (sincos), as the reference's g++ build merges
+/// them into glibc sincos.
 template <class T = Trig>
-ODEGPU_HD ODEGPU_INLINE void keller_miksis_rhs(Real tau, std::span<const Real> y, std::span<const Real> c,
-                                               std::span<Real> dy) {
-    const Real y1 = y[0], y2 = y[1];
-    if (!(y1 > 0)) {
-        dy[0] = std::numeric_limits<Real>::quiet_NaN();
-        dy[1] = std::numeric_limits<Real>::quiet_NaN();
-        return;
-    }
+ODEGPU_HD ODEGPU_INLINE void keller_miksis_time_terms(Real tau, std::span<const Real> c, std::span<Real> tt) {
     constexpr Real two_pi = 2.0 * 3.141592653589793238462643383279502884;
     const Real arg1 = two_pi * tau;
     const Real arg2 = two_pi * c[11] * tau + c[12];
     Real s1, c1, s2, c2;
     T::sincos(arg1, &s1, &c1);
     T::sincos(arg2, &s2, &c2);
+    tt[0] = c[5] * s1 + c[6] * s2;
+    tt[1] = c[7] * c1 + c[8] * c2;
+}
+
+/// Dimensionless Keller-Miksis RHS (keller_miksis.hpp:82-103) given its
+/// excitation terms, same operation order. y1 <= 0 yields NaN derivatives
+/// for the step control.
+ODEGPU_HD ODEGPU_INLINE void keller_miksis_rhs_split(std::span<const Real> y, std::span<const Real> c,
+                                                     std::span<const Real> tt, std::span<Real> dy) {
+    const Real y1 = y[0], y2 = y[1];
+    if (!(y1 > 0)) {
+        dy[0] = std::numeric_limits<Real>::quiet_NaN();
+        dy[1] = std::numeric_limits<Real>::quiet_NaN();
+        return;
+    }
 #if defined(__CUDA_ARCH__)
     // Every quotient of the RHS through the division fast path without its
     // per-division branch (1/y1, c3/y1 and c4 y2/y1 share one reciprocal of
@@ -59,8 +69,7 @@ ODEGPU_HD ODEGPU_INLINE void keller_miksis_rhs(Real tau, std::span<const Real> y
         pw = device::dmath::pow(inv, c[10]);
     }
     const Real numerator = (c[0] + c[1] * y2) * pw - c[2] * (1.0 + c[9] * y2) - q3 - q4 -
-                           (1.0 - third) * 1.5 * y2 * y2 - (c[5] * s1 + c[6] * s2) * (1.0 + c[9] * y2) -
-                           y1 * (c[7] * c1 + c[8] * c2);
+                           (1.0 - third) * 1.5 * y2 * y2 - tt[0] * (1.0 + c[9] * y2) - y1 * tt[1];
     const Real denominator = y1 - c[9] * y1 * y2 + c[4] * c[9];
     device::dmath::Divisor by_den(denominator);
     Real ddy = by_den.div(numerator);
@@ -70,12 +79,20 @@ ODEGPU_HD ODEGPU_INLINE void keller_miksis_rhs(Real tau, std::span<const Real> y
 #else
     const Real pw = std::pow(1.0 / y1, c[10]);
     const Real numerator = (c[0] + c[1] * y2) * pw - c[2] * (1.0 + c[9] * y2) - c[3] / y1 - c[4] * y2 / y1 -
-                           (1.0 - c[9] * y2 / 3.0) * 1.5 * y2 * y2 - (c[5] * s1 + c[6] * s2) * (1.0 + c[9] * y2) -
-                           y1 * (c[7] * c1 + c[8] * c2);
+                           (1.0 - c[9] * y2 / 3.0) * 1.5 * y2 * y2 - tt[0] * (1.0 + c[9] * y2) - y1 * tt[1];
     const Real denominator = y1 - c[9] * y1 * y2 + c[4] * c[9];
     dy[0] = y2;
     dy[1] = numerator / denominator;
 #endif
+}
+
+/// Dimensionless Keller-Miksis RHS (keller_miksis.hpp:82-103).
+template <class T = Trig>
+ODEGPU_HD ODEGPU_INLINE void keller_miksis_rhs(Real tau, std::span<const Real> y, std::span<const Real> c,
+                                               std::span<Real> dy) {
+    Real tt[2];
+    keller_miksis_time_terms<T>(tau, c, std::span<Real>(tt, 2));
+    keller_miksis_rhs_split(y, c, std::span<const Real>(tt, 2), dy);
 }
 
 /// KellerMiksisSystem (keller_miksis.hpp:106-119). Trig arguments 2 pi tau and
@@ -86,6 +103,15 @@ struct KellerMiksisHooksT : HookDefaults {
     using certified_hooks = KellerMiksisHooksT<CertifiedTrig>;
     ODEGPU_HD void ode_rhs(Real t, std::span<const Real> y, std::span<const Real> p, std::span<Real> dy) const {
         keller_miksis_rhs<T>(t, y, p, dy);
+    }
+    // time split (hooks.hpp TimeSplitHooks): the two excitation terms
+    static constexpr Index kTimeTermCount = 2;
+    ODEGPU_HD void time_terms(Real t, std::span<const Real> p, std::span<Real> tt) const {
+        keller_miksis_time_terms<T>(t, p, tt);
+    }
+    ODEGPU_HD void ode_rhs_split(Real, std::span<const Real> y, std::span<const Real> p, std::span<const Real> tt,
+                                 std::span<Real> dy) const {
+        keller_miksis_rhs_split(y, p, tt, dy);
     }
     ODEGPU_HD static Real trig_argument_bound(Real t0, Real t1, const Real* p, Index stride) {
         constexpr Real two_pi = 2.0 * 3.141592653589793238462643383279502884;

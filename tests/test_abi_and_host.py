@@ -136,3 +136,14 @@ def test_pool_accessors_and_errors():  # test_pool.cpp:46-67
         pool.state_at(0, 2)
     with pytest.raises(pkg.InvalidArgument):
         pkg.ProblemPool(pkg.PoolDims(0, 2, 3, 1))
+
+
+def test_time_split_models_match_their_rhs(tmp_path):
+    """hooks.hpp TimeSplitHooks: time_terms + ode_rhs_split == ode_rhs bit
+    for bit for the built-in split models (host compile of the same hooks)."""
+    root = abi.LIB_PATH.parents[2]
+    exe = tmp_path / "tts"
+    subprocess.run(["g++", "-std=c++20", "-O2", f"-I{root / 'include'}", str(root / "tests/cpp/test_time_split.cpp"),
+                    "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
