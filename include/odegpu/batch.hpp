@@ -115,6 +115,10 @@ public:
     Real param_at(Index i, Index c) const { return readable(kParams)[idx(i, c)]; }
     Real accessory_at(Index i, Index c) const { return readable(kAcc)[idx(i, c)]; }
 
+    /// Order in which the solve kernel takes up systems (ODEGPU_FETCH_*,
+    /// odegpu_batch_set_fetch_order); never changes a result.
+    void set_fetch_order(int mode) { detail::check(odegpu_batch_set_fetch_order(h_, mode)); }
+
     /// batch.cpp:42-44
     void reset_outcomes() {
         push();

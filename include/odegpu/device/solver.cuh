@@ -65,6 +65,9 @@ struct BatchArrays {
     Index n;                  // stride (batch capacity)
     Index count;              // systems [0, count) are integrated (count <= n)
     unsigned long long* work; // next system to hand out (zeroed before launch)
+    // fetch order: the j-th system handed out is order[j] (a permutation of
+    // [0, count)), or j when null (odegpu_batch_set_fetch_order)
+    const unsigned* order = nullptr;
     // Scan tallies (ScanDiagnostics, scan.hpp:41-49), accumulated across
     // solves when non-null: [5] detections, [6] detections outside their
     // zone, [7] max |F|/tolerance over detections (bits of a non-negative
@@ -762,11 +765,12 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
         // ================= PREPARE: bring this lane to a pending RK evaluation
         while (phase < kDone) {
             if (phase == kFetch) {
-                const Index sys = fetch_system(b.work);
-                if (sys >= b.count) {
+                const Index j = fetch_system(b.work);
+                if (j >= b.count) {
                     phase = kDone;
                     break;
                 }
+                const Index sys = b.order ? static_cast<Index>(__ldg(b.order + j)) : j;
                 if (b.reason[sys] == static_cast<std::uint8_t>(StopReason::NonFiniteAbort)) continue; // solve.hpp:98
                 ODEGPU_C(sys) = sys;
                 if constexpr (kCacheTT) ttc.clear(); // new parameters

@@ -24,6 +24,7 @@ ERR_CUDA = -3
 ERR_UNSUPPORTED = -4
 
 RK4, RKCK45 = 0, 1
+FETCH_NATURAL, FETCH_COST, FETCH_AUTO = 0, 1, 2  # odegpu_batch_set_fetch_order
 REACHED_END_TIME, EVENT_STOP, EQUILIBRIUM_STOP, NONFINITE_ABORT = 0, 1, 2, 3
 COPY_TIME_DOMAIN, COPY_ACTUAL_STATE, COPY_PARAMETER, COPY_ACCESSORIES, COPY_ALL = 0, 1, 2, 3, 4
 PROP_TIME_DOMAIN, PROP_STATE, PROP_PARAMETERS, PROP_ACCESSORIES = 0, 1, 2, 3
@@ -262,6 +263,7 @@ def _bind(lib):
         "odegpu_batch_destroy": (None, [vp]),
         "odegpu_batch_dims_get": (C.c_int, [vp, P(BatchDims)]),
         "odegpu_batch_set_stream": (C.c_int, [vp, vp]),
+        "odegpu_batch_set_fetch_order": (C.c_int, [vp, C.c_int32]),
         "odegpu_linear_set": (C.c_int, [vp, P(PoolView), P(LinearCopySpec)]),
         "odegpu_random_set": (C.c_int, [vp, P(PoolView), P(Index), P(Index), Index, C.c_int32]),
         "odegpu_batch_read": (C.c_int, [vp, C.c_int32, P(C.c_double)]),

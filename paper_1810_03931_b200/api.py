@@ -309,6 +309,10 @@ class SolverBatch:
     def set_stream(self, stream_handle: int | None):
         check(self._lib.odegpu_batch_set_stream(self._h, C.c_void_p(stream_handle or 0)))
 
+    def set_fetch_order(self, mode: int):
+        """abi.FETCH_NATURAL / FETCH_COST / FETCH_AUTO (odegpu_batch_set_fetch_order)."""
+        check(self._lib.odegpu_batch_set_fetch_order(self._h, mode))
+
     def sync(self):
         check(self._lib.odegpu_batch_sync(self._h))
 

@@ -234,6 +234,7 @@ void odegpu_batch_destroy(odegpu_batch* b) {
     cudaSetDevice(b->device);
     if (b->stream) cudaStreamSynchronize(b->stream);
     if (b->block) cudaFree(b->block);
+    if (b->order_block) cudaFree(b->order_block);
     if (b->host_flag) cudaFreeHost(b->host_flag);
     if (b->ev_start) cudaEventDestroy(b->ev_start);
     if (b->ev_stop) cudaEventDestroy(b->ev_stop);
@@ -257,6 +258,14 @@ int odegpu_batch_set_stream(odegpu_batch* b, void* stream) {
         DeviceGuard g(b->device);
         CK(cudaStreamSynchronize(b->stream));
         b->stream = stream ? static_cast<cudaStream_t>(stream) : b->own_stream;
+    });
+}
+
+int odegpu_batch_set_fetch_order(odegpu_batch* b, int32_t mode) {
+    return guarded([&] {
+        check_batch(b);
+        if (mode < ODEGPU_FETCH_NATURAL || mode > ODEGPU_FETCH_AUTO) throw_invalid("unknown fetch order mode");
+        b->order_mode = mode;
     });
 }
 

@@ -88,6 +88,12 @@ struct odegpu_batch {
     int64_t launches = 0;
     void* block = nullptr;     // single device allocation backing every array
     void* out_stage = nullptr; // lazily allocated pinned OutcomeStage for reads
+    // fetch order (odegpu_batch_set_fetch_order): a permutation of
+    // [0, order_count) built after each COST-mode solve (build_cost_order)
+    int32_t order_mode = ODEGPU_FETCH_AUTO;
+    odegpu::Index order_count = -1;
+    void* order_block = nullptr; // order + sort keys/values + CUB scratch
+    unsigned* order = nullptr;
 };
 
 namespace odegpu::detail {
@@ -108,6 +114,7 @@ void launch_scatter_rows(odegpu_batch* b, Real* dst, const Index* d_idx, const R
                          Index components);
 void enqueue_time_check(odegpu_batch* b); // solve.hpp:159-161 on [0, a.count)
 void launch_diagnostics(odegpu_batch* b);
+void build_cost_order(odegpu_batch* b); // longest-first fetch order from the last solve's trial steps
 void launch_tally(odegpu_batch* b, unsigned long long* tally, bool chunk_end); // scan outcome tally
 double run_dfma_peak(int blocks, int threads, int iters, double* seconds);
 

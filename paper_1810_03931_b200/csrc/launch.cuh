@@ -62,12 +62,23 @@ void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
         ++b->launches;
     }
     CK(cudaMemsetAsync(b->a.work, 0, sizeof(unsigned long long), b->stream));
+    // AUTO: longest-first for adaptive steppers of models whose policy asks
+    // for it (a fixed step count per system gives nothing to order)
+    constexpr bool kPolicyCost = [] {
+        if constexpr (requires { LaunchPolicy<H>::kCostOrder; })
+            return LaunchPolicy<H>::kCostOrder && ALG == Algorithm::RKCK45;
+        else return false;
+    }();
+    const bool cost = b->order_mode == ODEGPU_FETCH_COST || (b->order_mode == ODEGPU_FETCH_AUTO && kPolicyCost);
+    b->a.order = (cost && b->order_count == n) ? b->order : nullptr;
     CK(cudaEventRecord(b->ev_start, b->stream));
     kern<<<grid, kBlock, smem, b->stream>>>(hooks, b->a, c, b->first_bad);
     CK(cudaGetLastError());
     CK(cudaEventRecord(b->ev_stop, b->stream));
+    b->a.order = nullptr;
     b->timed = true;
     ++b->launches;
+    if (cost) build_cost_order(b); // for the next solve of this batch
 }
 
 template <class H>

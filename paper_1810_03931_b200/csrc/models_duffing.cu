@@ -18,6 +18,8 @@ namespace odegpu::detail {
 //   0.72 ms with the cold state in shared memory).
 // * the event / accessory RKCK45 models: cold state in shared memory frees
 //   enough registers (123 -> 72) for 7 blocks of 128 threads per SM.
+// * adaptive models take up systems longest first (kCostOrder, DESIGN.md
+//   §3.1): cfg2 2.09 -> 1.92 ms.
 template <>
 struct LaunchPolicy<models::DuffingMaxMinHooks> {
 #ifdef ODEGPU_CFG1_BLOCK
@@ -28,19 +30,23 @@ struct LaunchPolicy<models::DuffingMaxMinHooks> {
 template <>
 struct LaunchPolicy<models::DuffingMaxEventHooks> {
     static constexpr int kMinBlocks = ODEGPU_MB(6);
+    static constexpr bool kCostOrder = true;
 };
 template <>
 struct LaunchPolicy<models::DuffingMaxAccessoryHooks> {
     static constexpr int kMinBlocks = ODEGPU_MB(6);
+    static constexpr bool kCostOrder = true;
 };
 template <>
 struct LaunchPolicy<models::DuffingHooks> {
     static constexpr int kMinBlocks = ODEGPU_MB(6);
+    static constexpr bool kCostOrder = true;
 };
 // 4-dim Lyapunov system: 3 blocks/SM (<= 168 regs) keeps it spill-free.
 template <>
 struct LaunchPolicy<models::DuffingLyapunovHooks> {
     static constexpr int kMinBlocks = ODEGPU_MB(3);
+    static constexpr bool kCostOrder = true;
 };
 
 bool family_dims_duffing(const odegpu_model& m, odegpu_system_dims* d) {

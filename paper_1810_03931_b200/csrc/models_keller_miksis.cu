@@ -30,10 +30,12 @@ namespace odegpu::detail {
 template <>
 struct LaunchPolicy<models::BubbleCollapseHooks> {
     static constexpr int kMinBlocks = ODEGPU_MB(5);
+    static constexpr bool kCostOrder = true; // step counts spread widely: longest first
 };
 template <>
 struct LaunchPolicy<models::KellerMiksisHooks> {
     static constexpr int kMinBlocks = ODEGPU_MB(5);
+    static constexpr bool kCostOrder = true; // step counts spread widely: longest first
 };
 
 bool family_dims_keller_miksis(const odegpu_model& m, odegpu_system_dims* d) {

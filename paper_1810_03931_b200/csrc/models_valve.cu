@@ -21,6 +21,7 @@ namespace odegpu::detail {
 template <>
 struct LaunchPolicy<models::ValveHooks> {
     static constexpr int kMinBlocks = ODEGPU_MB(6);
+    static constexpr bool kCostOrder = true; // step counts spread widely: longest first
 };
 
 bool family_dims_valve(const odegpu_model& m, odegpu_system_dims* d) {

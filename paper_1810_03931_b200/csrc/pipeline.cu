@@ -361,6 +361,7 @@ void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
             s.start = start;
             s.count = n;
             b->a.count = n;
+            b->order_count = -1; // new systems: no cost order until this chunk's first solve
             // linear_set(All) of the chunk: pool -> batch (batch.cpp:78-104), on the copy-in stream
             copy_h2d_strided(b->a.td, cap, 0, j.pool->time_domain, N, start, n, 2, p->copy_in);
             copy_h2d_strided(b->a.state, cap, 0, j.pool->state, N, start, n, sd.system_dim, p->copy_in);

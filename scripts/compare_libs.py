@@ -1,7 +1,7 @@
 """Bitwise comparison of two builds of libodegpu on the BASELINE workloads
 (full size, a few iterations): proves that a kernel change that should not
 alter any value (e.g. the time-term cache) does not.
-Usage: python scripts/compare_libs.py run LIB OUT.npz [cfg ...]
+Usage: [FETCH=0|1|2] python scripts/compare_libs.py run LIB OUT.npz [cfg ...]
        python scripts/compare_libs.py diff A.npz B.npz"""
 import os, sys
 from pathlib import Path
@@ -14,7 +14,15 @@ sys.path.insert(0, str(ROOT / "tests"))
 if sys.argv[1] == "run":
     os.environ["ODEGPU_LIB"] = sys.argv[2]
     import parity
+    import paper_1810_03931_b200 as pkg
     from paper_1810_03931_b200 import workloads
+    if "FETCH" in os.environ:  # force a fetch order on every batch (abi.FETCH_*)
+        init = pkg.SolverBatch.__init__
+
+        def init_with_order(self, *a, **k):
+            init(self, *a, **k)
+            self.set_fetch_order(int(os.environ["FETCH"]))
+        pkg.SolverBatch.__init__ = init_with_order
     out = {}
     for name in sys.argv[4:] or ["cfg1", "cfg2", "cfg3", "cfg4"]:
         import time

@@ -1,6 +1,6 @@
 """Device time of one solve per config at full size (no torch): pristine batch
 restored before each run, kernel time from CUDA events on the batch stream.
-Usage: [ODEGPU_LIB=...] python scripts/quick_perf.py [cfg ...]"""
+Usage: [ODEGPU_LIB=...] [FETCH=0|1|2] python scripts/quick_perf.py [cfg ...]"""
 import json, os, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -14,6 +14,8 @@ for name in sys.argv[1:] or ["cfg2", "cfg3", "cfg4", "cfg1"]:
     pool = pkg.ProblemPool.from_arrays(td, y, p, acc)
     dims = pkg.make_batch_dims(wl.n, wl.model.dims())
     b, pristine = pkg.SolverBatch(dims), pkg.SolverBatch(dims)
+    if "FETCH" in os.environ:  # abi.FETCH_* (default: the model's policy)
+        b.set_fetch_order(int(os.environ["FETCH"]))
     pkg.linear_set(pristine, pool, pkg.LinearCopySpec(0, 0, wl.n))
     cfg = pkg.SolverConfig(wl.algorithm, wl.dt)
     runs = []
@@ -25,6 +27,6 @@ for name in sys.argv[1:] or ["cfg2", "cfg3", "cfg4", "cfg1"]:
         steps = d["accepted_steps"] + d["rejected_steps"]
         runs.append(dict(ms=round(ms, 3), steps=steps, frac=round(steps * wl.instr_per_step / (ms * 1e-3) / peak, 4)))
     best = min(runs[1:], key=lambda r: r["ms"])
-    print(json.dumps(dict(lib=os.path.basename(lib), name=name, n=wl.n, best_ms=best["ms"], steps=best["steps"],
+    print(json.dumps(dict(lib=os.path.basename(lib), fetch=os.environ.get("FETCH", "auto"), name=name, n=wl.n, best_ms=best["ms"], steps=best["steps"],
                           steps_per_s=best["steps"] / best["ms"] * 1e3, frac=best["frac"], peak=peak)), flush=True)
     b.close(); pristine.close()
