@@ -94,6 +94,7 @@ struct odegpu_batch {
     odegpu::Index order_count = -1;
     void* order_block = nullptr; // order + sort keys/values + CUB scratch
     unsigned* order = nullptr;
+    bool build_order = true; // false: the next solve's order would go unused (pipeline, last iteration)
 };
 
 namespace odegpu::detail {

@@ -78,7 +78,7 @@ void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
     b->a.order = nullptr;
     b->timed = true;
     ++b->launches;
-    if (cost) build_cost_order(b); // for the next solve of this batch
+    if (cost && b->build_order) build_cost_order(b); // for the next solve of this batch
 }
 
 template <class H>

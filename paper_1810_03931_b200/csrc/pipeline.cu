@@ -377,6 +377,7 @@ void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
             launch_reset_outcomes(b, 0, n);
             for (Index it = 0; it < j.iterations; ++it) {
                 enqueue_time_check(b);
+                b->build_order = it + 1 < j.iterations; // the chunk's last solve: its order would go unused
                 launch_model(b, p->model, j.cfg->algorithm, c);
                 if (tally) launch_tally(b, tally, false);
                 if (n_rec > 0 && it >= j.record_from) { // snapshots stay ordered with the kernels
