@@ -234,9 +234,9 @@ __device__ __forceinline__ void rhs_stage(const H& m, Real t, const Real (&y)[H:
 ///
 /// Time-split models (kTimeTerms<H> > 0, straight-line stages) go through
 /// the lane's time-term cache `tc` (TimeTermCache): the first stage reuses
-/// the terms at t if either slot holds them, and the step leaves the terms
-/// at t (slot 0: a rejected step's retry, a secant re-step) and at t + h
-/// (slot 1: the next step when this one is accepted) behind.
+/// the cached terms when their time equals t, and the step leaves the terms
+/// at its end point t + h behind (the next step's start once accepted; a
+/// two-slot policy also keeps those at t for a rejected step's retry).
 template <class H, Algorithm ALG, bool ROLLED, int BLOCK, bool OUTLINE, class TC>
 __device__ __forceinline__ bool rk_step(const H& m, Real t, Real h, const Real (&y)[H::kSystemDim],
                                         const Real* p, Real (&out)[H::kSystemDim],
@@ -482,7 +482,7 @@ constexpr int kMaxSecantIterations = 50; // events.hpp:190
 /// memory as structure of arrays (one column per thread, bank-conflict free)
 /// so that only the hot set — t, h, y, the step bookkeeping and the stage
 /// vectors — occupies registers; that is what sets occupancy.
-template <class H, int BLOCK, bool TT = false>
+template <class H, int BLOCK, int TT_SLOTS = 0>
 struct ColdState {
     static constexpr int N = H::kSystemDim;
     static constexpr int E = H::kEventCount > 0 ? H::kEventCount : 1;
@@ -505,30 +505,44 @@ struct ColdState {
     unsigned char clipped[BLOCK], relocated[BLOCK], s_conv[BLOCK], reason[BLOCK];
     // time-term cache of a time-split model (rk_step): slot s holds the
     // terms at tt_key[s]
-    static constexpr int TTB = TT ? BLOCK : 1;
-    Real tt_key[2][TTB];
-    Real tt_val[2][kTimeTerms<H> > 0 ? kTimeTerms<H> : 1][TTB];
+    static constexpr int TTB = TT_SLOTS > 0 ? BLOCK : 1;
+    static constexpr int TTS = TT_SLOTS > 0 ? TT_SLOTS : 1;
+    Real tt_key[TTS][TTB];
+    Real tt_val[TTS][kTimeTerms<H> > 0 ? kTimeTerms<H> : 1][TTB];
 };
 
 /// A lane's view of its time-term cache (two slots in its ColdState column).
-template <class CS, int K, bool ENABLED>
+template <class CS, int K, bool ENABLED, int SLOTS = 1>
 struct TimeTermCache {
     static constexpr bool kEnabled = ENABLED;
     CS& cs;
     int tid;
+    // two slots: [0] the terms at the step's start t (first stage), [1] at
+    // its end point t + h; one slot: only the end point, in [0]
     __device__ __forceinline__ bool lookup(Real t, Real (&tt)[K]) const {
-        const bool in1 = t == cs.tt_key[1][tid];
+        if constexpr (SLOTS == 1) {
 #pragma unroll
-        for (int i = 0; i < K; ++i) tt[i] = in1 ? cs.tt_val[1][i][tid] : cs.tt_val[0][i][tid];
-        return in1 || t == cs.tt_key[0][tid];
+            for (int i = 0; i < K; ++i) tt[i] = cs.tt_val[0][i][tid];
+            return t == cs.tt_key[0][tid];
+        } else {
+            const bool in1 = t == cs.tt_key[1][tid];
+#pragma unroll
+            for (int i = 0; i < K; ++i) tt[i] = in1 ? cs.tt_val[1][i][tid] : cs.tt_val[0][i][tid];
+            return in1 || t == cs.tt_key[0][tid];
+        }
     }
     __device__ __forceinline__ void store(int slot, Real key, const Real (&tt)[K]) const {
+        if constexpr (SLOTS == 1) {
+            if (slot == 0) return;
+            slot = 0;
+        }
         cs.tt_key[slot][tid] = key;
 #pragma unroll
         for (int i = 0; i < K; ++i) cs.tt_val[slot][i][tid] = tt[i];
     }
     __device__ __forceinline__ void clear() const {
-        cs.tt_key[0][tid] = cs.tt_key[1][tid] = __longlong_as_double(0x7ff8000000000000LL); // NaN
+#pragma unroll
+        for (int s = 0; s < SLOTS; ++s) cs.tt_key[s][tid] = __longlong_as_double(0x7ff8000000000000LL); // NaN
     }
 };
 
@@ -620,6 +634,17 @@ struct EffectivePolicy {
             return KernelPolicy<H>::kCacheTimeTerms && kTimeTerms<H> > 0 && !kRolledStages;
         else return kTimeTerms<H> > 0 && !kRolledStages;
     }();
+    // cache slots: 1 (the end point: the next step's start — measured best,
+    // cfg1 0.328 -> 0.314 ms, cfg3 13.0 -> 12.6 ms) or 2 (also a rejected
+    // step's retry start)
+    static constexpr int kTimeTermSlots = [] {
+#ifdef ODEGPU_POLICY_TT_SLOTS
+        if constexpr (true) return ODEGPU_POLICY_TT_SLOTS;
+        else
+#endif
+        if constexpr (requires { KernelPolicy<H>::kTimeTermSlots; }) return KernelPolicy<H>::kTimeTermSlots;
+        else return 1;
+    }();
     static constexpr int kParamStride = kParamsInShared ? (H::kParamCount | 1) : 1;
     static constexpr int kParamRegs = kParamsInShared ? 1 : (H::kParamCount > 0 ? H::kParamCount : 1);
 };
@@ -628,7 +653,7 @@ struct EffectivePolicy {
 /// memory: the Keller-Miksis layout exceeds the 48 KB static limit).
 template <class H, Algorithm ALG, int BLOCK, class Pol = EffectivePolicy<H>>
 struct SharedLayout {
-    ColdState<H, Pol::kColdInShared ? BLOCK : 1, Pol::kCacheTimeTerms> cold;
+    ColdState<H, Pol::kColdInShared ? BLOCK : 1, Pol::kCacheTimeTerms ? Pol::kTimeTermSlots : 0> cold;
     Bookkeeping<Pol::kBookInShared ? BLOCK : 1> book;
     Real params[Pol::kParamsInShared ? BLOCK * Pol::kParamStride : 1];
     Real k[Pol::kRolledStages ? (ALG == Algorithm::RK4 ? 3 : 5) * H::kSystemDim * BLOCK : 1];
@@ -665,13 +690,15 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
     // cold state: a shared-memory column per thread, or a register record
     extern __shared__ __align__(16) unsigned char odegpu_dsmem[];
     auto& sh = *reinterpret_cast<SharedLayout<H, ALG, BLOCK, Pol>*>(odegpu_dsmem);
-    ColdState<H, 1, Pol::kCacheTimeTerms> cs_regs;
+    ColdState<H, 1, Pol::kCacheTimeTerms ? Pol::kTimeTermSlots : 0> cs_regs;
     auto& cs = *[&] {
         if constexpr (Pol::kColdInShared) return &sh.cold;
         else return &cs_regs;
     }();
     const int tid = Pol::kColdInShared ? static_cast<int>(threadIdx.x) : 0;
-    const TimeTermCache<std::remove_reference_t<decltype(cs)>, (kTimeTerms<H> > 0 ? kTimeTerms<H> : 1), kCacheTT> ttc{
+    const TimeTermCache<std::remove_reference_t<decltype(cs)>, (kTimeTerms<H> > 0 ? kTimeTerms<H> : 1), kCacheTT,
+                        Pol::kTimeTermSlots>
+        ttc{
         cs, tid};
     if constexpr (kCacheTT) ttc.clear();
     Real* const sp = sh.params;

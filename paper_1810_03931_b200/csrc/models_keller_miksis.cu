@@ -10,18 +10,19 @@
 // rolled loop needed. With the bookkeeping in registers and the cold state +
 // 13 coefficients in shared memory (40 KB per block) 5 blocks of 128 fit per
 // SM: 15.5 -> 14.4 ms on cfg3 (rolled/inlined, 4 blocks) — DESIGN.md §3.1.
-// No time-term cache: its two slots (6 KB per block) would cost the fifth
-// block, and the outlined split adds a call per cached stage (15.1 ms).
+// The time-term cache keeps one slot (the step's end point, 3 KB per block):
+// 5 blocks still fit, 13.0 -> 12.6 ms; with two slots the fifth block is
+// lost (15.1 ms).
 namespace odegpu::device {
 template <>
 struct KernelPolicy<odegpu::models::BubbleCollapseHooks> {
     static constexpr bool kRolledStages = false, kColdInShared = true, kParamsInShared = true, kBookInShared = false,
-                          kOutlineRhs = true, kCacheTimeTerms = false;
+                          kOutlineRhs = true;
 };
 template <>
 struct KernelPolicy<odegpu::models::KellerMiksisHooks> {
     static constexpr bool kRolledStages = false, kColdInShared = true, kParamsInShared = true, kBookInShared = false,
-                          kOutlineRhs = true, kCacheTimeTerms = false;
+                          kOutlineRhs = true;
 };
 } // namespace odegpu::device
 
