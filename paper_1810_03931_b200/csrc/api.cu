@@ -6,10 +6,13 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_set>
 #include <vector>
+
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -140,6 +143,10 @@ odegpu_batch* batch_create(const odegpu_batch_dims& dims, int device) {
     auto* b = new odegpu_batch;
     b->dims = dims;
     b->device = device;
+    // tuning / experiment override of the default fetch order (0 natural,
+    // 1 cost, 2 auto) for batches the caller does not see (pipeline slots)
+    if (const char* env = std::getenv("ODEGPU_FETCH_ORDER"); env && env[0] >= '0' && env[0] <= '2' && !env[1])
+        b->order_mode = env[0] - '0';
     try {
         CK(cudaDeviceGetAttribute(&b->num_sms, cudaDevAttrMultiProcessorCount, device));
         CK(cudaStreamCreateWithFlags(&b->own_stream, cudaStreamNonBlocking));
