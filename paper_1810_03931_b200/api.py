@@ -362,12 +362,32 @@ def _controls(defn: SystemDef):
     return ode, ev
 
 
+_PREPARED: dict = {}
+
+
+def _prepared(defn: SystemDef, cfg: SolverConfig):
+    """The C structs of one (model, controls, config), built once per distinct
+    value: keyed on the values themselves, so mutating a model or config
+    between solves is picked up."""
+    o, e = defn.ode_controls(), defn.event_controls()
+    key = (type(defn), defn.model_id, tuple(defn.consts), tuple(o.rel_tol), tuple(o.abs_tol), o.max_step,
+           o.min_step, o.step_grow_limit, o.step_shrink_limit, tuple(e.direction), tuple(e.tolerance),
+           tuple(e.stop_condition), e.max_steps_in_zone, cfg.algorithm, cfg.initial_time_step, cfg.tile_size,
+           cfg.worker_count)
+    hit = _PREPARED.get(key)
+    if hit is None:
+        if len(_PREPARED) > 64:
+            _PREPARED.clear()
+        ode, ev = o.to_c(), e.to_c()
+        m, c = defn.to_c(), cfg.to_c()
+        hit = _PREPARED[key] = (C.byref(m), C.byref(c), C.byref(ode), C.byref(ev), (m, c, ode, ev))
+    return hit
+
+
 def solve(batch: SolverBatch, defn: SystemDef, cfg: SolverConfig | None = None):
     """solve.hpp:60-128 — synchronous, in place."""
-    cfg = cfg or SolverConfig()
-    ode, ev = _controls(defn)
-    check(batch._lib.odegpu_solve(batch.handle, C.byref(defn.to_c()), C.byref(cfg.to_c()), C.byref(ode),
-                                  C.byref(ev)))
+    m, c, ode, ev, _ = _prepared(defn, cfg or SolverConfig())
+    check(batch._lib.odegpu_solve(batch.handle, m, c, ode, ev))
 
 
 def solve_iteratively(batch: SolverBatch, defn: SystemDef, cfg: SolverConfig | None, iterations: int, sink=None):
