@@ -393,8 +393,7 @@ def solve(batch: SolverBatch, defn: SystemDef, cfg: SolverConfig | None = None):
 def solve_iteratively(batch: SolverBatch, defn: SystemDef, cfg: SolverConfig | None, iterations: int, sink=None):
     """solve.hpp:133-142. sink(iteration, batch) after each solve; with no
     sink the iterations run back to back on the device."""
-    cfg = cfg or SolverConfig()
-    ode, ev = _controls(defn)
+    m, c, ode, ev, _ = _prepared(defn, cfg or SolverConfig())
     err = []
 
     def _sink(it, _h, _u):
@@ -406,8 +405,7 @@ def solve_iteratively(batch: SolverBatch, defn: SystemDef, cfg: SolverConfig | N
             return 1
 
     cb = abi.SINK(_sink) if sink else abi.SINK()
-    rc = batch._lib.odegpu_solve_iteratively(batch.handle, C.byref(defn.to_c()), C.byref(cfg.to_c()),
-                                             C.byref(ode), C.byref(ev), int(iterations), cb, None)
+    rc = batch._lib.odegpu_solve_iteratively(batch.handle, m, c, ode, ev, int(iterations), cb, None)
     if err:
         raise err[0]
     check(rc)
