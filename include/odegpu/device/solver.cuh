@@ -68,6 +68,9 @@ struct BatchArrays {
     // fetch order: the j-th system handed out is order[j] (a permutation of
     // [0, count)), or j when null (odegpu_batch_set_fetch_order)
     const unsigned* order = nullptr;
+    // when non-null: each finished system's RK evaluations (trial steps +
+    // secant re-steps), the key of the next fetch order
+    unsigned* cost = nullptr;
     // Scan tallies (ScanDiagnostics, scan.hpp:41-49), accumulated across
     // solves when non-null: [5] detections, [6] detections outside their
     // zone, [7] max |F|/tolerance over detections (bits of a non-negative
@@ -500,6 +503,7 @@ struct ColdState {
     Real th_prev[BLOCK], f_prev[BLOCK], th_cur[BLOCK], f_cur[BLOCK], th_min[BLOCK], b_th[BLOCK], b_f[BLOCK];
     long long sys[BLOCK];
     unsigned n_det[BLOCK], n_secf[BLOCK];
+    unsigned n_resteps[BLOCK]; // secant re-steps of the current system (its cost beyond the trial steps)
     int counter[E][BLOCK];
     int s_it[BLOCK], s_idx[BLOCK], located[BLOCK];
     unsigned char clipped[BLOCK], relocated[BLOCK], s_conv[BLOCK], reason[BLOCK];
@@ -810,7 +814,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
 #pragma unroll
                 for (int i = 0; i < NA; ++i) acc[i] = b.acc[sys + i * n];
                 ODEGPU_B(n_acc) = ODEGPU_B(n_rej) = 0u;
-                ODEGPU_C(n_det) = ODEGPU_C(n_secf) = 0u;
+                ODEGPU_C(n_det) = ODEGPU_C(n_secf) = ODEGPU_C(n_resteps) = 0u;
                 ODEGPU_B(smallest) = __longlong_as_double(0x7ff0000000000000LL); // +inf
                 ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::ReachedEndTime);
                 // driver.hpp:96-107
@@ -935,6 +939,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 b.rejected[sys] = ODEGPU_B(n_rej);
                 b.detections[sys] = ODEGPU_C(n_det);
                 b.secant_failures[sys] = ODEGPU_C(n_secf);
+                if (b.cost) b.cost[sys] = ODEGPU_B(n_acc) + ODEGPU_B(n_rej) + ODEGPU_C(n_resteps);
                 b.smallest_step[sys] = ODEGPU_B(smallest);
                 phase = kFetch;
                 continue;
@@ -1135,6 +1140,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
             else setup_step(false);
         } else if (phase == kReadySecant) { // one secant iteration's step is in (events.hpp:222-240)
             if constexpr (E > 0) {
+                ++ODEGPU_C(n_resteps);
                 Real fs[EE];
                 m.event_values(t + h_step, CS(yn, N), CS(prow, NP), S(fs, E));
                 const int s_idx = ODEGPU_C(s_idx);

@@ -94,6 +94,7 @@ struct odegpu_batch {
     odegpu::Index order_count = -1;
     void* order_block = nullptr; // order + sort keys/values + CUB scratch
     unsigned* order = nullptr;
+    unsigned* cost = nullptr; // per-system RK evaluations of the last COST-mode solve (BatchArrays::cost)
     bool build_order = true; // false: the next solve's order would go unused (pipeline, last iteration)
 };
 
@@ -115,7 +116,9 @@ void launch_scatter_rows(odegpu_batch* b, Real* dst, const Index* d_idx, const R
                          Index components);
 void enqueue_time_check(odegpu_batch* b); // solve.hpp:159-161 on [0, a.count)
 void launch_diagnostics(odegpu_batch* b);
-void build_cost_order(odegpu_batch* b); // longest-first fetch order from the last solve's trial steps
+// longest-first fetch order from the last solve's RK evaluations (its cost
+// array when the kernel wrote it, else accepted + rejected steps)
+void build_cost_order(odegpu_batch* b, bool have_cost);
 void launch_tally(odegpu_batch* b, unsigned long long* tally, bool chunk_end); // scan outcome tally
 double run_dfma_peak(int blocks, int threads, int iters, double* seconds);
 

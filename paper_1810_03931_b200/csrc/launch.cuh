@@ -71,14 +71,17 @@ void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
     }();
     const bool cost = b->order_mode == ODEGPU_FETCH_COST || (b->order_mode == ODEGPU_FETCH_AUTO && kPolicyCost);
     b->a.order = (cost && b->order_count == n) ? b->order : nullptr;
+    b->a.cost = (cost && b->build_order) ? b->cost : nullptr; // null until the first order build allocates it
     CK(cudaEventRecord(b->ev_start, b->stream));
     kern<<<grid, kBlock, smem, b->stream>>>(hooks, b->a, c, b->first_bad);
     CK(cudaGetLastError());
     CK(cudaEventRecord(b->ev_stop, b->stream));
     b->a.order = nullptr;
+    const bool have_cost = b->a.cost != nullptr;
+    b->a.cost = nullptr;
     b->timed = true;
     ++b->launches;
-    if (cost && b->build_order) build_cost_order(b); // for the next solve of this batch
+    if (cost && b->build_order) build_cost_order(b, have_cost); // for the next solve of this batch
 }
 
 template <class H>
