@@ -47,3 +47,20 @@ def test_rejects_unknown_mode():
     with pytest.raises(pkg.InvalidArgument):
         b.set_fetch_order(7)
     b.close()
+
+
+def test_scan_pipeline_rows_independent_of_fetch_order(monkeypatch):
+    """Pipeline slots take their mode from ODEGPU_FETCH_ORDER at creation:
+    a valve scan (iterations 2.. of every chunk longest-first under AUTO)
+    gives bitwise the rows of the same scan in index order."""
+    from paper_1810_03931_b200 import scan
+
+    def run(mode):
+        monkeypatch.setenv("ODEGPU_FETCH_ORDER", str(mode))
+        spec = scan.ValveScanSpec(q=scan.ParamRange(0.2, 10.0, 6000), transient=24, saved=4,
+                                  solver=scan.SolveOptions(rel_tol=1e-10, abs_tol=1e-10, batch_capacity=2048))
+        return scan.run_valve_scan(spec)
+
+    a, b = run(abi.FETCH_NATURAL), run(abi.FETCH_AUTO)
+    assert a.rows.tobytes() == b.rows.tobytes()
+    assert a.diagnostics == b.diagnostics
