@@ -263,6 +263,34 @@ int main() {
         CHECK(cb.accessory_at(0, 0) == cb.state_at(0, 0));
     });
 
+    run_case("fetch order changes no result (set_fetch_order)", [] {
+        models::DuffingMaxEventSystem def(1e-6, 0);
+        const Index n = 3000;
+        ProblemPool pool(PoolDims{n, 2, 4, 2});
+        for (Index i = 0; i < n; ++i) {
+            pool.time_end(i) = 2.0 * std::numbers::pi;
+            pool.param_at(i, 0) = 0.2 + 0.1 * Real(i % 50) / 49.0; // k
+            pool.param_at(i, 1) = 0.1 + 0.4 * Real(i / 50) / 59.0;  // B
+            pool.param_at(i, 2) = 1.0;                                // delta
+            pool.param_at(i, 3) = 1.0;                                // omega
+        }
+        SolverBatch a(make_batch_dims(n, def.dims())), b(make_batch_dims(n, def.dims()));
+        a.set_fetch_order(ODEGPU_FETCH_NATURAL);
+        b.set_fetch_order(ODEGPU_FETCH_COST);
+        linear_set(a, pool, {0, 0, n, CopyMode::All});
+        linear_set(b, pool, {0, 0, n, CopyMode::All});
+        solve_iteratively(a, def, SolverConfig{}, 3, [](Index, const SolverBatch&) {});
+        solve_iteratively(b, def, SolverConfig{}, 3, [](Index, const SolverBatch&) {});
+        const SolverBatch &ca = a, &cb = b;
+        bool same = true;
+        for (Index i = 0; i < n; ++i)
+            same = same && ca.state_at(i, 0) == cb.state_at(i, 0) && ca.state_at(i, 1) == cb.state_at(i, 1) &&
+                   ca.accessory_at(i, 0) == cb.accessory_at(i, 0) &&
+                   ca.outcomes()[std::size_t(i)].rejected_steps == cb.outcomes()[std::size_t(i)].rejected_steps;
+        CHECK(same);
+        CHECK_THROWS_AS(a.set_fetch_order(9), std::invalid_argument);
+    });
+
     run_case("bubble scan smoke: every iteration stops at a located maximum", [] { // test_scan.cpp:176-196
         // 1 (pa1) x 1 (pa2) x 2 (f1) x 3 (f2) grid, 8 transient + 4 saved iterations
         const std::vector<Real> f1 = {20.0, 1000.0}, f2 = {20.0, 141.42135623730951, 1000.0};
