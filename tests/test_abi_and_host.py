@@ -155,3 +155,14 @@ def test_time_split_models_match_their_rhs(tmp_path):
                     "-o", str(exe)], check=True)
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_c_header_is_plain_c11(tmp_path):
+    """include/odegpu.h is the drop-in boundary: it must compile as strict C11
+    (no C++ or CUDA types in the signatures)."""
+    root = abi.LIB_PATH.parents[2]
+    src = tmp_path / "hc.c"
+    src.write_text('#include "odegpu.h"\nint main(void) { return ODEGPU_FETCH_AUTO == 2 ? 0 : 1; }\n')
+    r = subprocess.run(["gcc", "-std=c11", "-Wall", "-Wextra", "-pedantic", "-Werror", f"-I{root / 'include'}",
+                        "-c", str(src), "-o", str(tmp_path / "hc.o")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
