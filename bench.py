@@ -2,39 +2,50 @@
 """Benchmark of the ensemble-solve hot path (BASELINE.json metric: FP64 RK
 steps/s and systems/s, % of FP64 peak, vs the host CPU).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5 --log2n 24]
     python bench.py --impl reference ...   # the reference CPU solver arm
 
-A "step" is one solve() over the whole batch (one solve_iteratively
-iteration). Default workload: BASELINE.json configs[1] — Duffing RKCK45 with
-the local-maximum EventFunction and event-time accessories on a 1024 x 1024
-(damping x forcing) grid of 2^20 systems.
+Default workload: BASELINE.json configs[4] at its largest single-GPU size —
+the Keller-Miksis scaling pool of 2^24 systems (4096 PA1 x 4096 f1, RKCK45
+tol 1e-10, BubbleCollapseSystem), iterated IN PLACE the way the reference's
+run_bubble_scan drives it (src/scan.cpp:247-329 -> solve_iteratively,
+solve.hpp:133-142): every step is one solve() over the whole pool that
+continues from the previous step's end point (one collapse per system).
 
-* value: trial steps (accepted + rejected, counted on the device) per second
-  of device time with the batch resident in HBM; timed with CUDA events on the
-  batch's stream around each solve, L2 flushed (256 MiB write) between steps
-  outside the events.
-* e2e: the same metric through the C ABI with host (pinned) buffers: the
-  chunked pool pipeline (odegpu_pipeline_run, 8 chunks, copy-in / kernels /
-  copy-out streams overlapped) — H2D of the pool, solve, D2H of time
-  domains / state / accessories / outcome records into host arrays, per
-  step, wall-clock.
-* roofline: FP64-pipe lane instructions per trial step (SURVEY.md §8d
-  algorithmic count) / solve-kernel time vs the DFMA microbenchmark peak.
+* value: trial steps (accepted + rejected, counted on the device) per second,
+  pool resident in HBM. Timed with ONE pair of CUDA events on the batch stream
+  around all K steps (plus the per-step device outcome tally), bracketed by a
+  barrier + synchronize; max over ranks. The pool (3.3 GB at 2^24) is larger
+  than L2, so no flush is needed between steps.
+* fetch order: lanes take systems longest first by their cost in the
+  PREVIOUS iteration (AUTO policy) — information a real scan has. cfg2 cannot
+  iterate in place (the reference's secant Zeno loop): every
+  step restarts from the initial conditions and runs in natural order.
+* e2e: the same metric through the C ABI with host (pinned) buffers — the
+  chunked pool pipeline (odegpu_pipeline_run): per step H2D of the pool, one
+  in-place iteration, D2H of the end points and outcome records into the
+  host pool, wall clock.
+* roofline: FP64-pipe instructions per trial step (SURVEY.md §8d algorithmic
+  count) x device-counted trial steps / solve-kernel time vs the DFMA
+  microbenchmark peak measured in the same run.
 * cpu_baseline: the reference solver (oracle/_ref, compiled from the
-  reference's own sources) timed on this box's host cores on a bounded
-  strided sample of the same workload.
+  reference's own sources) on this box's host cores, bounded sample.
 
-Multi-GPU (torchrun): weak scaling; rank r owns rows [r*1024, (r+1)*1024) of a
-(1024*N) x 1024 grid; no collective on the data path; the barrier and a MAX
-all-reduce of the timed region are the only communication.
+Multi-GPU (torchrun, or `--gpus N` which relaunches itself under torchrun):
+STRONG scaling of the same fixed pool. Rank r owns the blocks b of 4096
+systems with b % N == r (block-cyclic: every rank samples the whole grid, so
+the per-rank work is balanced without any exchange); no collective on the data
+path — the barrier and MAX/SUM all-reduces of the timing are the only
+communication.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -50,24 +61,27 @@ from paper_1810_03931_b200 import abi, workloads  # noqa: E402
 
 METRIC = "FP64 RK trial steps/s"
 UNIT = "steps/s"
+BLOCK = 4096  # block-cyclic ownership granule of the multi-rank split
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2", choices=sorted(workloads.CONFIGS) + ["cfg5"])
+    ap.add_argument("--config", default="cfg5", choices=sorted(workloads.CONFIGS) + ["cfg5"])
     ap.add_argument("--log2n", type=int, default=24, help="cfg5: Keller-Miksis pool of 2^log2n systems")
-    ap.add_argument("--strong", action="store_true",
-                    help="cfg5 under torchrun: the 2^log2n pool is split over the ranks (default: each rank "
-                         "integrates 2^log2n systems)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-chunks", type=int, default=0, help="pipeline chunks for e2e (0 = by pool size)")
     ap.add_argument("--cpu-sample", type=int, default=0, help="systems in the CPU sample (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--no-natural", action="store_true", help="skip the natural-order comparison solve")
+    ap.add_argument("--partition", default="cyclic", choices=["cyclic", "contiguous"],
+                    help="multi-rank split: block-cyclic (balanced) or contiguous slices (odegpu_slice)")
+    ap.add_argument("--allow-shared-gpu", action="store_true",
+                    help="let more ranks than GPUs share devices (tests only; the rate is then shared too)")
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -77,29 +91,41 @@ def dist_env():
     return rank, world, local
 
 
-def make_workload(name: str, rank: int, world: int, args=None):
-    """Rank-local slice of the weak-scaling grid (cfg5 --strong: a contiguous
-    slice of one fixed pool, odegpu_slice's split)."""
-    if name == "cfg5":
-        wl = workloads.cfg5(args.log2n)
-        if world > 1 and args.strong:
-            lo, hi = pkg.slice_range(wl.n, world, rank)
-            wl = wl.subset(slice(lo, hi))
-            wl.description += f"; rank {rank}/{world} slice [{lo}, {hi}) (strong scaling)"
-        elif world > 1:
-            wl.description += f"; rank {rank}/{world} replica (weak scaling)"
-        return wl
-    if name == "cfg2" and world > 1:
-        full_k = workloads.param_range(0.2, 0.3, 1024 * world)
-        wl = workloads.cfg2(1024, 1024)
-        k = np.repeat(full_k[rank * 1024:(rank + 1) * 1024], 1024)
-        wl.p[0] = k
-        wl.description += f"; rank {rank}/{world} slice of a {1024 * world}x1024 grid"
-        return wl
-    wl = workloads.CONFIGS[name]()
-    if world > 1:  # replicate other configs with a disjoint shift of the first parameter row
-        wl.description += f"; rank {rank}/{world} replica"
-    return wl
+def relaunch_under_torchrun(args) -> int:
+    """`python bench.py --gpus N` without torchrun: one process per GPU."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def full_workload(args):
+    return workloads.cfg5(args.log2n) if args.config == "cfg5" else workloads.CONFIGS[args.config]()
+
+
+def workload_name(args, wl):
+    return f"cfg5_keller_miksis_2^{args.log2n}" if args.config == "cfg5" else wl.name
+
+
+def owned_indices(n: int, rank: int, world: int, partition: str) -> np.ndarray:
+    """Systems rank `rank` integrates: block-cyclic blocks of BLOCK, or the
+    contiguous odegpu_slice share."""
+    if world == 1:
+        return np.arange(n)
+    if partition == "contiguous":
+        lo, hi = pkg.slice_range(n, world, rank)
+        return np.arange(lo, hi)
+    blocks = np.arange(rank, -(-n // BLOCK), world)
+    idx = (blocks[:, None] * BLOCK + np.arange(BLOCK)[None, :]).reshape(-1)
+    return idx[idx < n]
+
+
+def in_place(config: str) -> bool:
+    """cfg2 restarts every step (the reference's own solver hits a Zeno loop
+    when its grid is iterated in place); the rest iterate."""
+    return config != "cfg2"
 
 
 class ClockSampler:
@@ -168,61 +194,101 @@ def load_traffic(name: str):
         return None
 
 
-def cpu_baseline(wl, sample: int, iterations: int = 1):
-    """Reference solver (oracle/_ref) on all host cores, bounded strided sample."""
+def host_info() -> dict:
+    """CPU model, physical cores and the threads this process may use (lscpu)."""
+    info = {"threads_available": len(os.sched_getaffinity(0))}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {}
+        for line in out.splitlines():
+            if ":" in line:
+                k, v = line.split(":", 1)
+                kv[k.strip()] = v.strip()
+        info["cpu_model"] = kv.get("Model name")
+        cps, sockets = kv.get("Core(s) per socket"), kv.get("Socket(s)")
+        if cps and sockets and cps.isdigit() and sockets.isdigit():
+            info["physical_cores"] = int(cps) * int(sockets)
+        info["logical_cpus"] = int(kv["CPU(s)"]) if kv.get("CPU(s)", "").isdigit() else None
+    except Exception:
+        pass
+    return info
+
+
+def reference_rate(wl, sample: int, warmup: int, steps: int, workers: int, in_place_iter: bool):
+    """The reference solver (oracle/_ref) on a strided sample of the workload,
+    stepped exactly like the GPU arm: `warmup` untimed iterations, then
+    `steps` timed ones (in place, or each from the initial conditions)."""
+    from oracle import pyoracle
+
+    sub = wl.strided(sample)
+    td, y, p, acc = sub.arrays()
+    oc = abi.empty_outcomes(sub.n)
+    kw = dict(algorithm=sub.algorithm, dt=sub.dt, iterations=1, workers=workers, outcomes=oc)
+    for _ in range(warmup):
+        if not in_place_iter:
+            td, y, p, acc = sub.arrays()
+            oc[:] = abi.empty_outcomes(sub.n)
+        pyoracle.solve("reference", sub.model, td, y, p, acc, **kw)
+    total_steps, total_s = 0, 0.0
+    for _ in range(steps):
+        if not in_place_iter:
+            td, y, p, acc = sub.arrays()
+            oc[:] = abi.empty_outcomes(sub.n)
+        _, secs, _ = pyoracle.solve("reference", sub.model, td, y, p, acc, **kw)
+        total_steps += int(oc["accepted_steps"].sum() + oc["rejected_steps"].sum())
+        total_s += secs
+    return total_steps / total_s, sub.n * steps / total_s, sub.n, total_s
+
+
+def cpu_baseline(wl, args, sample: int):
+    """Reference solver on all host threads (bounded sample) plus a 1-thread
+    figure on a smaller sample, with the CPU model and core counts."""
     from oracle import pyoracle
 
     if not pyoracle.available("reference"):
         return None
-    cores = pyoracle.host_cores()
-    sub = wl.strided(sample)
-    r = pyoracle.solve_workload("reference", sub, iterations, workers=cores)
-    steps = int(r["outcomes"]["accepted_steps"].sum() + r["outcomes"]["rejected_steps"].sum())
-    # outcomes hold the last iteration only; scale by iterations for the rate
-    rate = steps * iterations / r["seconds"]
-    return {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
-            "sample": f"{sub.n} of {wl.n} systems (evenly strided), {iterations} solve() iteration(s), "
-                      f"{r['seconds']:.2f} s wall, ODENSEMBLE worker_count={cores}",
-            "systems_per_s": sub.n * iterations / r["seconds"]}
+    info = host_info()
+    threads = info["threads_available"]
+    ip = in_place(args.config)
+    rate, sys_rate, n_s, secs = reference_rate(wl, sample, 1, 2, threads, ip)
+    rate1, _, n_1, secs1 = reference_rate(wl, max(sample // max(threads, 1), 256), 1, 1, 1, ip)
+    return {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{n_s} of {wl.n} systems (evenly strided), 1 untimed + 2 timed "
+                      f"{'in-place iterations' if ip else 'solves from the initial conditions'}, "
+                      f"{secs:.2f} s timed, reference solve() with worker_count={threads}",
+            "systems_per_s": sys_rate,
+            "one_thread": {"value": rate1, "sample": f"{n_1} systems, 1 timed iteration, {secs1:.2f} s"},
+            "host": info}
 
 
 def run_reference_arm(args, rank, world):
-    """--impl reference: the reference CPU solver on this box's host cores."""
+    """--impl reference: the reference CPU solver on this box's host cores,
+    same metric and config as our arm (bounded sample per step)."""
     if rank != 0:
         return
     from oracle import pyoracle
 
-    wl = workloads.cfg5(args.log2n) if args.config == "cfg5" else workloads.CONFIGS[args.config]()
+    wl = full_workload(args)
     if not pyoracle.available("reference"):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libodref.so not built"}))
         return
-    cores = pyoracle.host_cores()
-    sample = args.cpu_sample or {"cfg1": 46080, "cfg2": 1 << 20, "cfg3": 1 << 17, "cfg4": 1 << 18,
-                                 "cfg5": 1 << 17}[args.config]
-    sub = wl.strided(sample)
-    # like the GPU arm, every step solves the sample from its initial
-    # conditions (iterating cfg2 in place hits the reference's secant Zeno
-    # loop from the 3rd period on, DESIGN.md §4)
-    for _ in range(args.warmup):
-        td, y, p, acc = sub.arrays()
-        pyoracle.solve("reference", sub.model, td, y, p, acc, algorithm=sub.algorithm, dt=sub.dt, iterations=1,
-                       workers=cores)
-    total_steps, total_s = 0, 0.0
-    for _ in range(args.steps):
-        td, y, p, acc = sub.arrays()
-        oc, secs, _ = pyoracle.solve("reference", sub.model, td, y, p, acc, algorithm=sub.algorithm, dt=sub.dt,
-                                     iterations=1, workers=cores)
-        total_steps += int(oc["accepted_steps"].sum() + oc["rejected_steps"].sum())
-        total_s += secs
-    value = total_steps / total_s
-    desc = f"{sub.n} of {wl.n} systems (evenly strided) per step, reference solve() on {cores} threads"
+    info = host_info()
+    threads = info["threads_available"]
+    sample = args.cpu_sample or {"cfg1": 46080, "cfg2": 1 << 19, "cfg3": 1 << 16, "cfg4": 1 << 17,
+                                 "cfg5": 1 << 16}[args.config]
+    ip = in_place(args.config)
+    value, sys_rate, n_s, total_s = reference_rate(wl, sample, args.warmup, args.steps, threads, ip)
+    desc = (f"{n_s} of {wl.n} systems (evenly strided) per step, "
+            f"{'iterated in place' if ip else 'each step from the initial conditions'}, "
+            f"reference solve() on {threads} threads")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl.name, "description": wl.description, "sample": desc},
-        "systems_per_s": sub.n * args.steps / total_s,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": desc},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args, wl), "description": wl.description, "sample": desc},
+        "systems_per_s": sys_rate,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": desc,
+                         "host": info},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
@@ -234,16 +300,28 @@ def log(msg: str):
     print(f"[bench +{time.time() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
 
 
+def pinned_like(torch, a: np.ndarray) -> np.ndarray:
+    """A page-locked copy of `a` (numpy view of pinned torch storage)."""
+    buf = torch.empty(max(a.size, 1), dtype=torch.float64, pin_memory=True).numpy()[: a.size]
+    buf[:] = a
+    return buf
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     if world > 1:
+        import torch
         import torch.distributed as dist
 
-        import torch
-
-        # one rank per GPU: NCCL; ranks sharing a GPU (single-GPU test runs): gloo
         shared = torch.cuda.device_count() < world
+        if shared and args.impl == "ours" and not args.allow_shared_gpu:
+            if rank == 0:
+                print(json.dumps({"error": f"{world} ranks but {torch.cuda.device_count()} visible GPUs "
+                                           "(pass --allow-shared-gpu to share devices in a test)"}))
+            sys.exit(2)
         dist.init_process_group("nccl" if args.impl == "ours" and not shared else "gloo")
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
@@ -258,9 +336,22 @@ def main():
     device = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(device)
     red_dev = f"cuda:{device}" if world > 1 and torch.distributed.get_backend() == "nccl" else "cpu"
-    log(f"torch ready, rank {rank}/{world} on cuda:{local}")
-    wl = make_workload(args.config, rank, world, args)
+    log(f"torch ready, rank {rank}/{world} on cuda:{device}")
+
+    def allreduce(vals, op):
+        if world == 1:
+            return vals
+        import torch.distributed as dist
+
+        t = torch.tensor(vals, dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t, op=op)
+        return [float(v) for v in t.tolist()]
+
+    full = full_workload(args)
+    mine = owned_indices(full.n, rank, world, args.partition)
+    wl = full if world == 1 else full.subset(mine)
     n = wl.n
+    ip = in_place(args.config)
     td, y, p, acc = wl.arrays()
     pool = pkg.ProblemPool.from_arrays(td, y, p, acc)
     batch = pkg.SolverBatch(pkg.make_batch_dims(n, wl.model.dims()), device=device)
@@ -268,121 +359,110 @@ def main():
     batch.set_stream(stream.cuda_stream)
     cfg = pkg.SolverConfig(wl.algorithm, wl.dt)
     pkg.linear_set(batch, pool, pkg.LinearCopySpec(0, 0, n))
-    # Every step integrates the synthetic batch from its initial conditions:
-    # a pristine copy stays resident in HBM and is restored device-to-device
-    # outside the timed events. (Iterating cfg2 in place is not an option:
-    # from the 3rd forcing period on, 5 of its 2^20 systems enter a
-    # secant/relocation Zeno loop — theta clamps to h*1e-12 forever — in the
-    # reference solver itself.)
-    pristine = pkg.SolverBatch(pkg.make_batch_dims(n, wl.model.dims()), device=device)
-    pkg.batch_copy(pristine, batch)
+    pristine = None
+    if not ip:  # cfg2: every step from the initial conditions, natural order
+        pristine = pkg.SolverBatch(pkg.make_batch_dims(n, wl.model.dims()), device=device)
+        pkg.batch_copy(pristine, batch)
+        batch.set_fetch_order(abi.FETCH_NATURAL)
 
-    log(f"{wl.name}: {n} systems resident")
+    log(f"{wl.name}: {n} of {full.n} systems resident on this rank")
     peak_lane, _ = pkg.dfma_peak(device)
     log(f"DFMA peak {peak_lane:.4e} lane-DFMA/s")
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{device}")
 
-    for _ in range(args.warmup):
-        pkg.batch_copy(batch, pristine)
+    for _ in range(args.warmup):  # the scan's first (transient) iterations
+        if pristine is not None:
+            pkg.batch_copy(batch, pristine)
         pkg.solve(batch, wl.model, cfg)
 
-    # ---------------- timed region (device-resident batch)
+    # ---------------- timed region (device-resident pool)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     launches0 = batch.launch_count()
-    ev_ms, kern_ms, steps_total, sys_total, max_trial = [], [], 0, 0, 0
+    kern_ms, steps_total, max_trial, certified = [], 0, 0, False
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
     with ClockSampler(device) as clocks:
+        w0 = time.perf_counter()
+        e_start.record(stream)
         for _ in range(args.steps):
-            pkg.batch_copy(batch, pristine)  # initial conditions, outside the events
-            with torch.cuda.stream(stream):
-                flush.fill_(1)  # L2 flush between steps, outside the events
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
+            if pristine is not None:  # restore outside the kernel-time events (inside the span)
+                pkg.batch_copy(batch, pristine)
             pkg.solve(batch, wl.model, cfg)
-            e1.record(stream)
-            e1.synchronize()
-            ev_ms.append(e0.elapsed_time(e1))
             kern_ms.append(batch.last_kernel_ms())
-            certified = batch.trig_certified()
             d = batch.diagnostics()
             steps_total += d["accepted_steps"] + d["rejected_steps"]
             max_trial = max(max_trial, d["max_trial_steps"])
-            sys_total += n
-    launches = batch.launch_count() - launches0 - args.steps  # minus the diagnostics tallies
+        e_end.record(stream)
+        e_end.synchronize()
+        wall = time.perf_counter() - w0
+        certified = batch.trig_certified()
     torch.cuda.synchronize()
-    elapsed = sum(ev_ms) / 1e3
+    launches = batch.launch_count() - launches0 - args.steps  # minus the outcome tallies
+    span_s = e_start.elapsed_time(e_end) / 1e3
     kernel_s = sum(kern_ms) / 1e3
-    if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([elapsed, kernel_s], dtype=torch.float64, device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed, kernel_s = float(t[0]), float(t[1])
-        c = torch.tensor([steps_total, sys_total], dtype=torch.float64, device=red_dev)
-        dist.all_reduce(c, op=dist.ReduceOp.SUM)
-        steps_total, sys_total = int(c[0]), int(c[1])
-
-    value = steps_total / elapsed
+    my_steps = steps_total
+    span_s, kernel_s, wall = allreduce([span_s, kernel_s, wall], torch.distributed.ReduceOp.MAX if world > 1 else None)
+    steps_total, sys_total = allreduce([steps_total, n * args.steps],
+                                       torch.distributed.ReduceOp.SUM if world > 1 else None)
+    steps_total, sys_total = int(steps_total), int(sys_total)
+    value = steps_total / span_s
     achieved = steps_total * wl.instr_per_step / kernel_s  # lane FP64-pipe instr/s (all ranks)
     peak_total = peak_lane * world
+    log(f"timed region done: {steps_total} trial steps in {span_s:.4f} s (kernels {kernel_s:.4f} s)")
 
-    log(f"timed region done: {steps_total} trial steps in {elapsed:.4f} s")
-    # the same solve in natural fetch order (outside the timed region), for
-    # the fetch_order note in config: the timed steps take up systems
-    # longest-first by the previous solve's trial steps (AUTO policy)
-    cost_order = wl.algorithm == abi.RKCK45
-    natural_ms = None
-    if cost_order:
+    # ---------------- the same iteration in natural fetch order (outside the
+    # timed region): a snapshot of the pool is solved once ordered, once not
+    natural = None
+    if ip and wl.algorithm == abi.RKCK45 and not args.no_natural:
+        snap = pkg.SolverBatch(pkg.make_batch_dims(n, wl.model.dims()), device=device)
+        pkg.batch_copy(snap, batch)
+        pkg.solve(batch, wl.model, cfg)
+        ordered_ms = batch.last_kernel_ms()
+        pkg.batch_copy(batch, snap)
         batch.set_fetch_order(abi.FETCH_NATURAL)
-        pkg.batch_copy(batch, pristine)
         pkg.solve(batch, wl.model, cfg)
         natural_ms = batch.last_kernel_ms()
-        batch.set_fetch_order(abi.FETCH_AUTO)
+        d = batch.diagnostics()
+        st = d["accepted_steps"] + d["rejected_steps"]
+        natural = {"ordered_kernel_ms": ordered_ms, "natural_kernel_ms": natural_ms,
+                   "frac_natural_order": st * wl.instr_per_step / (natural_ms / 1e3) / peak_lane,
+                   "frac_previous_iteration_order": st * wl.instr_per_step / (ordered_ms / 1e3) / peak_lane}
+        snap.close()
+    batch.close()
+    if pristine is not None:
+        pristine.close()
+
     # ---------------- e2e: through the C ABI with host buffers, per step
-    h_td = torch.empty(2 * n, dtype=torch.float64, pin_memory=True).numpy()
-    h_y = torch.empty(y.size, dtype=torch.float64, pin_memory=True).numpy()
-    h_p = torch.empty(p.size, dtype=torch.float64, pin_memory=True).numpy()
-    h_a = torch.empty(max(acc.size, 1), dtype=torch.float64, pin_memory=True).numpy()[: acc.size]
-    h_td[:], h_y[:], h_p[:], h_a[:] = td, y, p, acc
+    h_td, h_y, h_p, h_a = (pinned_like(torch, a) for a in (td, y, p, acc))
     pin_pool = pkg.ProblemPool.from_arrays(td, y, p, acc)
     pin_pool._td, pin_pool._state, pin_pool._params, pin_pool._acc = h_td, h_y, h_p, h_a
-    o_y = torch.empty(y.size, dtype=torch.float64, pin_memory=True).numpy()
-    o_td = torch.empty(2 * n, dtype=torch.float64, pin_memory=True).numpy()
-    o_a = torch.empty(max(acc.size, 1), dtype=torch.float64, pin_memory=True).numpy()[: acc.size]
-    lib = abi.load()
-    h2d = (h_td.nbytes + h_y.nbytes + h_p.nbytes + h_a.nbytes)
-    d2h = o_y.nbytes + o_td.nbytes + o_a.nbytes + n * abi.OUTCOME_DTYPE.itemsize
-    e2e_steps, e2e_s = 0, 0.0
     outc = torch.zeros(n * abi.OUTCOME_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True).numpy().view(
         abi.OUTCOME_DTYPE)
-    if world > 1:
-        torch.distributed.barrier()
-    # the chunked pool pipeline: chunks through a 3-stage copy-in / kernels /
-    # copy-out pipeline (odegpu_pipeline_run); device batches and pinned
-    # staging are allocated once, like a scan driver would. Chunk count
-    # (scripts/e2e_chunks.py): ~64 Ki systems per chunk, 2..8 chunks for the
-    # transfer-bound cheap models, up to 16 for Keller-Miksis
+    h2d = h_td.nbytes + h_y.nbytes + h_p.nbytes + h_a.nbytes
+    d2h = h_td.nbytes + h_y.nbytes + h_a.nbytes + outc.nbytes
+    # chunks through the copy-in / kernels / copy-out pipeline (in place: end
+    # points go back into the pool arrays). ~64 Ki systems per chunk, 2..8
+    # chunks for the transfer-bound cheap models, up to 16 for Keller-Miksis
+    # (scripts/e2e_chunks.py)
     n_chunks = args.e2e_chunks or int(min(max(round(n / 65536), 2), 16 if wl.instr_per_step > 500 else 8))
     cap = max(1, -(-n // n_chunks))
     pipe = pkg.api.Pipeline(wl.model, cap, device)
-    outs = (o_td, o_y, o_a, outc)
-    pipe.run(pin_pool, cfg, 1, out_arrays=outs)  # warm-up (first-touch of the output pages)
-    for _ in range(args.e2e_steps):
-        t0 = time.perf_counter()
-        pipe.run(pin_pool, cfg, 1, out_arrays=outs)
-        e2e_s += time.perf_counter() - t0
-        e2e_steps += int(outc["accepted_steps"].sum() + outc["rejected_steps"].sum())
-    pipe.close()
+    outs = (h_td, h_y, h_a, outc) if ip else (pinned_like(torch, td), pinned_like(torch, y),
+                                              pinned_like(torch, acc), outc)
+    pipe.run(pin_pool, cfg, 1, out_arrays=outs)  # warm-up (first touch of the staging)
     if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([e2e_s, e2e_steps], dtype=torch.float64, device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t[0])
-        e2e_steps = e2e_steps * world  # weak scaling: every rank did its share
+        torch.distributed.barrier()
+    e2e_steps, t0 = 0, time.perf_counter()
+    for _ in range(args.e2e_steps):
+        pipe.run(pin_pool, cfg, 1, out_arrays=outs)
+        e2e_steps += int(outc["accepted_steps"].sum() + outc["rejected_steps"].sum())
+    e2e_s = time.perf_counter() - t0
+    pipe.close()
+    (e2e_s,) = allreduce([e2e_s], torch.distributed.ReduceOp.MAX if world > 1 else None)
+    (e2e_steps,) = allreduce([e2e_steps], torch.distributed.ReduceOp.SUM if world > 1 else None)
     e2e_value = e2e_steps / e2e_s
+    log(f"e2e done ({e2e_value:.4e} steps/s)")
 
     if rank != 0:
         if world > 1:
@@ -392,15 +472,15 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        sample = args.cpu_sample or {"cfg1": 46080, "cfg2": 1 << 20, "cfg3": 1 << 18, "cfg4": 1 << 19,
-                                     "cfg5": 1 << 18}[args.config]
-        log(f"e2e done ({e2e_value:.4e} steps/s); CPU baseline on {sample} systems")
-        cpu = cpu_baseline(wl, sample)
+        sample = args.cpu_sample or {"cfg1": 46080, "cfg2": 1 << 19, "cfg3": 1 << 16, "cfg4": 1 << 17,
+                                     "cfg5": 1 << 16}[args.config]
+        log(f"CPU baseline on {sample} systems")
+        cpu = cpu_baseline(full, args, sample)
 
     traffic = load_traffic(wl.name)
     per_launch_s = kernel_s / args.steps
-    hbm_bytes = n * 8 * (2 * 2 + 2 * wl.model.dims().system_dim + wl.model.dims().param_count
-                         + 2 * wl.model.dims().accessory_count) + n * 49
+    dims = wl.model.dims()
+    hbm_bytes = n * 8 * (2 * 2 + 2 * dims.system_dim + dims.param_count + 2 * dims.accessory_count) + n * 49
     out = {
         "metric": METRIC,
         "value": value,
@@ -408,33 +488,38 @@ def main():
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": 1e3 * elapsed / args.steps,
+        "ms_per_step": 1e3 * span_s / args.steps,
         "higher_is_better": True,
-        "scaling": "strong" if (args.config == "cfg5" and args.strong) else "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
         "config": {
-            "workload": wl.name if args.config != "cfg5" else f"cfg5_keller_miksis_2^{args.log2n}",
-            "description": wl.description,
+            "workload": workload_name(args, wl),
+            "description": full.description,
+            "systems": full.n,
             "systems_per_gpu": n,
-            "step": "one solve() over the batch (one forcing period for cfg1/cfg2, one collapse / section-to-"
-                    "section iteration for cfg3/cfg4)",
+            "step": ("one in-place solve() iteration of the whole pool (solve_iteratively; one collapse / "
+                     "forcing period / section-to-section iteration per system)") if ip else
+                    "one solve() of the whole pool from its initial conditions (one forcing period)",
             "algorithm": "RK4" if wl.algorithm == abi.RK4 else "RKCK45",
-            "l2": "flushed between steps (256 MiB write outside the timed events)",
-            "parallelism": f"replicas{world}" if world > 1 else "single GPU",
+            "l2": ("inputs larger than L2 (pool of %.2f GB resident in HBM), no flush" % (hbm_bytes / 1e9)),
+            "parallelism": (f"dp{world}: block-cyclic {BLOCK}-system blocks per rank" if args.partition == "cyclic"
+                            else f"dp{world}: contiguous slices") if world > 1 else "single GPU",
             "trig_path": "certified (branch-free, include/odegpu/trig.hpp)" if certified else "general",
-            "fetch_order": ("longest first by each system's trial steps in the batch's previous solve (AUTO "
-                            "policy; here the previous timed step, i.e. the same solve: exact costs. Ordered by "
-                            "the previous iteration of an in-place scan instead, the gain is 5-7% rather than "
-                            "8-11% - DESIGN.md 3.1)") if cost_order else "natural (fixed step: equal costs)",
-            "natural_order_kernel_ms": natural_ms,
+            "fetch_order": ("longest first by each system's RK evaluations in the PREVIOUS iteration (AUTO "
+                            "policy, what an in-place scan knows)") if ip and wl.algorithm == abi.RKCK45 else
+                           "natural (index order)",
+            "natural_order": natural,
+            "library": os.environ.get("ODEGPU_LIB") or ("parity" if os.environ.get("ODEGPU_BUILD") == "parity"
+                                                         else "libodegpu.so (fast build)"),
         },
-        "systems_per_s": sys_total / elapsed,
+        "systems_per_s": sys_total / span_s,
         "trial_steps_per_system_step": steps_total / max(sys_total, 1),
         "max_trial_steps_one_system": max_trial,
         "gpu_launches": launches,
         "kernel_ms_per_step": 1e3 * per_launch_s,
+        "wall_s_timed_region": wall,
         "roofline": {
             "bound": "fp64",
             "achieved": achieved / 1e9,
@@ -448,13 +533,14 @@ def main():
             "peak_source": "DFMA microbenchmark in this run (odegpu_dfma_peak, 8 independent chains/thread); "
                            "MEASURED_PEAKS.json has no FP64 entry",
             "tflops_fp64": steps_total * wl.flops_per_step / kernel_s / 1e12,
-            "hbm_gbs": hbm_bytes / per_launch_s / 1e9,
+            "hbm_gbs": hbm_bytes * world / per_launch_s / 1e9,
         },
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "steps": args.e2e_steps,
-                "path": f"odegpu_pipeline_run over the pinned host pool: {n_chunks} chunks, H2D / kernels / D2H of td, "
-                        "state, accessories and outcome records on separate streams (4 chunks in flight), "
-                        "into host arrays, wall-clock"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d) * world,
+                "d2h_bytes_per_step": int(d2h) * world, "steps": args.e2e_steps,
+                "path": f"odegpu_pipeline_run over the pinned host pool: {n_chunks} chunks per rank, H2D / "
+                        "kernels / D2H of td, state, accessories and outcome records on separate streams, "
+                        + ("one in-place iteration per step (end points written back into the pool), "
+                           if ip else "") + "wall clock, max over ranks"},
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
     }

@@ -223,7 +223,10 @@ __device__ __forceinline__ void rhs_stage(const H& m, Real t, const Real (&y)[H:
 /// One trial step from (t, y) with step h (steppers.hpp:82-139). Writes the
 /// proposed state, the embedded error |y5 - y4| (RKCK45) and whether
 /// anything is non-finite. Expressions are those of the reference, operation
-/// for operation.
+/// for operation — but the default build lets nvcc contract a*b+c into one
+/// DFMA (one rounding instead of two), which the reference's g++ build
+/// without -march never does; only the parity build (make parity,
+/// -fmad=false) rounds every product and sum separately like the reference.
 ///
 /// ROLLED: the stages are a rolled loop around ONE inlined RHS call site; a
 /// uniform switch on the stage index forms the stage argument from the
@@ -1039,7 +1042,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     h_next = smax(h_try * c.step_shrink_limit, c.min_step);
                 } else {
                     accepted = ratio <= 1.0;
-                    Real factor = 0.9 * dmath::pow_neg_fifth(ratio); // std::pow(ratio, -0.2)
+                    Real factor = 0.9 * dmath::controller_pow(ratio); // std::pow(ratio, -0.2)
                     factor = sclamp(factor, c.step_shrink_limit, c.step_grow_limit);
                     h_next = sclamp(h_try * factor, c.min_step, c.max_step);
                     if (!accepted && h_try <= c.min_step) {

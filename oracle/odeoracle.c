@@ -718,6 +718,24 @@ int odo_rhs(const odegpu_model* mdesc, double t, const double* y, const double* 
     return 0;
 }
 
+/* ode_rhs of n systems (SoA, stride n) at per-system times t[i]: the parity
+ * checker's event slopes dF/dt at full pool sizes (tests/parity.py). */
+int odo_rhs_batch(const odegpu_model* mdesc, odegpu_index n, const double* t, const double* y, const double* p,
+                  odegpu_index dim, odegpu_index np, double* dy) {
+    Model m;
+    int rc = model_init(&m, mdesc);
+    if (rc) return rc;
+    double yi[8], pi[16], di[8];
+    if (dim > 8 || np > 16) return fail(ODEGPU_ERR_INVALID_ARGUMENT, "rhs_batch: model too wide");
+    for (odegpu_index i = 0; i < n; ++i) {
+        for (odegpu_index c = 0; c < dim; ++c) yi[c] = y[i + c * n];
+        for (odegpu_index c = 0; c < np; ++c) pi[c] = p[i + c * n];
+        ode_rhs(&m, t[i], yi, pi, di);
+        for (odegpu_index c = 0; c < dim; ++c) dy[i + c * n] = di[c];
+    }
+    return 0;
+}
+
 /* keller_miksis.hpp:47-77 */
 int odo_bubble_coefficients(odegpu_index n, const double* phys, double* out) {
     for (odegpu_index i = 0; i < n; ++i) {

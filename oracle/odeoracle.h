@@ -40,6 +40,8 @@ int odo_locate_secant(const odegpu_model* m, int algorithm, double t, const doub
                       double* theta, double* value, int* converged);
 /* models: rhs and bubble coefficients */
 int odo_rhs(const odegpu_model* m, double t, const double* y, const double* p, double* dy);
+int odo_rhs_batch(const odegpu_model* m, odegpu_index n, const double* t, const double* y, const double* p,
+                  odegpu_index dim, odegpu_index np, double* dy);
 int odo_bubble_coefficients(odegpu_index n, const double* phys, double* out);
 const char* odo_last_error(void);
 

@@ -64,6 +64,9 @@ def load(which: str) -> C.CDLL:
                                               C.c_double, C.c_int, C.c_double, C.c_double, C.c_double, C.c_void_p,
                                               C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int)]
             lib.odo_rhs.restype = C.c_int
+            lib.odo_rhs_batch.restype = C.c_int
+            lib.odo_rhs_batch.argtypes = [C.POINTER(abi.Model), abi.Index, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          abi.Index, abi.Index, C.c_void_p]
             lib.odo_rhs.argtypes = [C.POINTER(abi.Model), C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]
         _libs[which] = lib
     return _libs[which]

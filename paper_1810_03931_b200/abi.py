@@ -15,6 +15,10 @@ import numpy as np
 PKG_DIR = Path(__file__).resolve().parent
 LIB_DIR = PKG_DIR / "lib"
 LIB_PATH = LIB_DIR / "libodegpu.so"
+# the exact-parity build (make parity: -fmad=false, libdevice pow in the
+# step controller); selected with ODEGPU_BUILD=parity or ODEGPU_LIB=<path>
+PARITY_LIB_PATH = LIB_DIR / "libodegpu_parity.so"
+BUILD_PARITY = 1  # odegpu_build_flags() bit
 
 # include/odegpu.h constants
 OK = 0
@@ -256,6 +260,7 @@ def _bind(lib):
     vp = C.c_void_p
     sig = {
         "odegpu_abi_version": (C.c_int, []),
+        "odegpu_build_flags": (C.c_int, []),
         "odegpu_last_error": (C.c_char_p, []),
         "odegpu_device_count": (C.c_int, []),
         "odegpu_model_dims": (C.c_int, [P(Model), P(SystemDims)]),
@@ -339,7 +344,8 @@ def load() -> C.CDLL:
     """Load the in-tree libodegpu.so (fails loudly if it was not built)."""
     global _lib
     if _lib is None:
-        path = Path(os.environ.get("ODEGPU_LIB", LIB_PATH))
+        default = PARITY_LIB_PATH if os.environ.get("ODEGPU_BUILD") == "parity" else LIB_PATH
+        path = Path(os.environ.get("ODEGPU_LIB", default))
         if not path.exists():
             raise LibraryMissing(
                 f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`"

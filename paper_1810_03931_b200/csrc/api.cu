@@ -208,6 +208,14 @@ extern "C" {
 
 int odegpu_abi_version(void) { return ODEGPU_ABI_VERSION; }
 
+int odegpu_build_flags(void) {
+#if defined(ODEGPU_PARITY_BUILD) && ODEGPU_PARITY_BUILD
+    return ODEGPU_BUILD_PARITY;
+#else
+    return 0;
+#endif
+}
+
 const char* odegpu_last_error(void) { return g_err.c_str(); }
 
 int odegpu_device_count(void) {

@@ -112,7 +112,8 @@ def compare(wl, gpu, ref, *, pinned_state=(), pinned_acc=(), time_acc=()) -> dic
 def event_slope(wl, ref, idx):
     """|dF0/dt| at the reference's stop points; F0 = y2 for every stop event
     of the workloads (duffing.hpp:136, keller_miksis.hpp:324, valve.hpp:435),
-    so dF0/dt = dy2/dt from the model RHS (evaluated by the C oracle)."""
+    so dF0/dt = dy2/dt from the model RHS (evaluated by the C oracle, one
+    batched call)."""
     import ctypes as C
 
     from oracle import pyoracle
@@ -120,17 +121,15 @@ def event_slope(wl, ref, idx):
     lib = pyoracle.load("port")
     d = wl.model.dims()
     n = wl.n
-    y = ref["y"].reshape(d.system_dim, n)
-    p = wl.p.reshape(d.param_count, n) if d.param_count else None
-    out = np.empty(idx.size)
-    m = C.byref(wl.model.to_c())
-    for j, i in enumerate(idx):
-        yi = np.ascontiguousarray(y[:, i])
-        pi = np.ascontiguousarray(p[:, i]) if p is not None else np.zeros(1)
-        dy = np.zeros(d.system_dim)
-        lib.odo_rhs(m, float(ref["outcomes"]["final_t"][i]), abi.vptr(yi), abi.vptr(pi), abi.vptr(dy))
-        out[j] = abs(dy[1])
-    return out
+    k = idx.size
+    y = np.ascontiguousarray(ref["y"].reshape(d.system_dim, n)[:, idx])
+    p = (np.ascontiguousarray(wl.p.reshape(d.param_count, n)[:, idx]) if d.param_count else np.zeros(1))
+    t = np.ascontiguousarray(ref["outcomes"]["final_t"][idx], dtype=np.float64)
+    dy = np.zeros((d.system_dim, k))
+    rc = lib.odo_rhs_batch(C.byref(wl.model.to_c()), k, abi.vptr(t), abi.vptr(y), abi.vptr(p), d.system_dim,
+                           d.param_count, abi.vptr(dy))
+    assert rc == 0
+    return np.abs(dy[1])
 
 
 # Per-config comparison rules: which components a stop event

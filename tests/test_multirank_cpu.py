@@ -1,11 +1,11 @@
 """World-size-2 gloo test of the multi-GPU host logic on CPU.
 
 Systems are independent, so the multi-GPU path has no data-path collective:
-each rank owns the contiguous slice odegpu_slice(N, world, rank) and the
-results are gathered on the host. Here each rank integrates its slice with
-the C oracle (no GPU needed), the slices are all-gathered over gloo and must
-reproduce the single-process run bitwise; bench.py's weak-scaling workload
-split is checked the same way.
+each rank owns a share of the pool and the results are gathered on the host.
+Here each rank integrates its share with the C oracle standing in for its
+device (no GPU here), the shares are all-gathered over gloo and must
+reproduce the single-process run bitwise — for the contiguous odegpu_slice
+split and for bench.py's block-cyclic strong-scaling split.
 """
 import os
 import socket
@@ -41,14 +41,16 @@ def _worker(rank, world, port, out_q):
         r = pyoracle.solve_workload("port", mine, 2)
         gathered = [None] * world
         dist.all_gather_object(gathered, (b, e, r["y"], r["outcomes"]["accepted_steps"]))
-        # bench.py weak-scaling split of the cfg2 grid
+        # bench.py's strong-scaling split: block-cyclic blocks of bench.BLOCK
         import bench
 
-        wl2 = bench.make_workload("cfg2", rank, world)
-        rows = [None] * world
-        dist.all_gather_object(rows, wl2.p[0][::1024].copy())
+        wl2 = workloads.cfg4().strided(3 * bench.BLOCK + 77)
+        idx = bench.owned_indices(wl2.n, rank, world, "cyclic")
+        r2 = pyoracle.solve_workload("port", wl2.subset(idx), 1)
+        cyc = [None] * world
+        dist.all_gather_object(cyc, (idx, r2["y"], r2["outcomes"]["accepted_steps"]))
         if rank == 0:
-            out_q.put((gathered, rows))
+            out_q.put((gathered, cyc))
     finally:
         dist.destroy_process_group()
 
@@ -65,7 +67,7 @@ def test_two_rank_slices_reproduce_single_process_run():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    gathered, rows = q.get(timeout=240)
+    gathered, cyc = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -85,6 +87,20 @@ def test_two_rank_slices_reproduce_single_process_run():
     assert np.array_equal(steps, full["outcomes"]["accepted_steps"])
     assert pkg.slice_range(600, 2, 0) == (0, 300) and pkg.slice_range(601, 2, 1) == (301, 601)
 
-    # weak scaling: rank r owns k-rows [r*1024, (r+1)*1024) of a 2048 x 1024 grid
-    k_all = np.concatenate(rows)
-    assert np.array_equal(k_all, workloads.param_range(0.2, 0.3, 2048))
+    # block-cyclic: the ranks' shares partition the pool and reassemble the
+    # single-process run bitwise
+    import bench
+
+    wl2 = workloads.cfg4().strided(3 * bench.BLOCK + 77)
+    full2 = pyoracle.solve_workload("port", wl2, 1)
+    owner = np.full(wl2.n, -1)
+    y2 = np.empty((dim, wl2.n))
+    s2 = np.empty(wl2.n, dtype=np.int64)
+    for r, (idx, ys, st) in enumerate(cyc):
+        assert np.all(owner[idx] == -1)
+        owner[idx] = r
+        y2[:, idx] = ys.reshape(dim, idx.size)
+        s2[idx] = st
+    assert np.all(owner >= 0)
+    assert np.array_equal(y2.reshape(-1).view(np.uint64), full2["y"].view(np.uint64))
+    assert np.array_equal(s2, full2["outcomes"]["accepted_steps"])
