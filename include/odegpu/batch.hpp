@@ -5,13 +5,20 @@
 //
 // Coherence protocol per array (time domain, state, parameters,
 // accessories, outcomes):
-//   * const accessors copy device -> host only if the mirror is stale;
-//   * non-const accessors additionally mark the device copy stale (the
-//     caller may write through the span); it is re-uploaded before the next
-//     device operation;
+//   * const accessors copy device -> host only if the mirror is stale; the
+//     span they return is a snapshot, valid until the next device operation
+//     (re-acquire it afterwards);
+//   * non-const accessors hand out a span into live storage, as the
+//     reference's do (batch.hpp:24-34): from then on the array is LIVE — it is
+//     uploaded before every device operation and downloaded right after every
+//     device operation that modifies it, so writes through a span taken before
+//     a solve() reach the device and the span shows the solve's results, as
+//     with the reference's host vectors. detach_spans() ends that (outstanding
+//     mutable spans must then be re-acquired) and returns to lazy transfers;
 //   * device operations (linear_set, random_set, solve) invalidate the
 //     mirror of what they modify.
-// Transient iterations therefore cost no PCIe traffic unless a sink reads.
+// Transient iterations therefore cost no PCIe traffic unless a sink reads or
+// a mutable span is outstanding.
 #ifndef ODEGPU_BATCH_HPP
 #define ODEGPU_BATCH_HPP
 
@@ -102,6 +109,7 @@ public:
     std::span<SystemOutcome> outcomes() {
         pull_outcomes();
         dirty_[kOut] = true;
+        live_[kOut] = true;
         return outcomes_;
     }
     std::span<const SystemOutcome> outcomes() const {
@@ -126,22 +134,37 @@ public:
         valid_[kOut] = false;
     }
 
-    /// Upload every array the host modified (before a device operation).
+    /// Upload every array the host modified or may have modified through an
+    /// outstanding mutable span (before a device operation).
     void push() {
         for (int k = 0; k < 4; ++k)
-            if (dirty_[k]) {
-                detail::check(odegpu_batch_write(h_, k, host_[k].data()));
+            if (dirty_[k] || live_[k]) {
+                if (!host_[k].empty()) detail::check(odegpu_batch_write(h_, k, host_[k].data()));
                 dirty_[k] = false;
             }
-        if (dirty_[kOut]) {
+        if (dirty_[kOut] || live_[kOut]) {
             detail::check(odegpu_batch_write_outcomes(h_, reinterpret_cast<const odegpu_outcome*>(outcomes_.data())));
             dirty_[kOut] = false;
         }
     }
-    /// The device modified arrays `mask` (bit k = array k, bit 4 = outcomes).
+    /// The device modified arrays `mask` (bit k = array k, bit 4 = outcomes):
+    /// live arrays are refreshed now (their spans must show the new values),
+    /// the others on their next access.
     void invalidate_host(unsigned mask) {
         for (int k = 0; k < 5; ++k)
-            if (mask & (1u << k)) valid_[k] = false;
+            if (mask & (1u << k)) {
+                valid_[k] = false;
+                if (live_[k]) {
+                    if (k == kOut) pull_outcomes();
+                    else readable(k);
+                }
+            }
+    }
+    /// Mutable spans handed out so far become invalid (re-acquire them);
+    /// transfers go back to lazy (see the coherence protocol above).
+    void detach_spans() {
+        push();
+        for (bool& l : live_) l = false;
     }
 
 private:
@@ -159,6 +182,7 @@ private:
     std::span<Real> writable(int k) {
         readable(k);
         dirty_[k] = true;
+        live_[k] = true;
         return host_[k];
     }
     void pull_outcomes() const {
@@ -175,6 +199,7 @@ private:
         for (int k = 0; k < 5; ++k) {
             std::swap(valid_[k], o.valid_[k]);
             std::swap(dirty_[k], o.dirty_[k]);
+            std::swap(live_[k], o.live_[k]);
         }
     }
 
@@ -184,6 +209,7 @@ private:
     mutable std::vector<SystemOutcome> outcomes_;
     mutable bool valid_[5] = {true, true, true, true, true}; // fresh batch: zeros on both sides
     bool dirty_[5] = {false, false, false, false, false};
+    bool live_[5] = {false, false, false, false, false}; // a mutable span is outstanding
 };
 
 /// batch.cpp:78-104 — pool[start_in_pool, +n) -> batch[start_in_batch, +n).

@@ -46,7 +46,7 @@ ODEGPU_HD ODEGPU_INLINE void keller_miksis_rhs_split(std::span<const Real> y, st
         dy[1] = std::numeric_limits<Real>::quiet_NaN();
         return;
     }
-#if defined(__CUDA_ARCH__)
+#if defined(__CUDA_ARCH__) && !ODEGPU_GLIBM
     // Every quotient of the RHS through the division fast path without its
     // per-division branch (1/y1, c3/y1 and c4 y2/y1 share one reciprocal of
     // y1; /3 uses RN(1/3)) and pow in its branch-free form — bitwise the
@@ -77,7 +77,9 @@ ODEGPU_HD ODEGPU_INLINE void keller_miksis_rhs_split(std::span<const Real> y, st
     dy[0] = y2;
     dy[1] = ddy;
 #else
-    const Real pw = std::pow(1.0 / y1, c[10]);
+    // host, and the exact-parity build: the reference's expression with its
+    // libm's pow (glibc restated on the device, include/odegpu/device/glibm.h)
+    const Real pw = libm_pow(1.0 / y1, c[10]);
     const Real numerator = (c[0] + c[1] * y2) * pw - c[2] * (1.0 + c[9] * y2) - c[3] / y1 - c[4] * y2 / y1 -
                            (1.0 - c[9] * y2 / 3.0) * 1.5 * y2 * y2 - tt[0] * (1.0 + c[9] * y2) - y1 * tt[1];
     const Real denominator = y1 - c[9] * y1 * y2 + c[4] * c[9];

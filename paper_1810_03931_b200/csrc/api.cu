@@ -332,6 +332,9 @@ int odegpu_random_set(odegpu_batch* b, const odegpu_pool_view* pool, const odegp
         if (copy_mode < ODEGPU_COPY_TIME_DOMAIN || copy_mode > ODEGPU_COPY_ALL)
             throw_invalid("random_set: unknown copy mode");
         if (count == 0) return;
+        for (int32_t prop = 0; prop <= ODEGPU_PROP_ACCESSORIES; ++prop) // before any allocation
+            if (wants(copy_mode, prop) && components_of(b->dims, prop) > 0 && !pool_ptr(pool, prop))
+                throw_invalid("random_set: pool array missing");
         DeviceGuard g(b->device);
         const Index np = pool->dims.problem_size;
         // gather on the host into one staging block, one H2D, scatter on device
@@ -614,7 +617,7 @@ extern "C" int odegpu_custom_end(odegpu_batch* b) {
 extern "C" int odegpu_math_check(int fn, odegpu_index n, const double* x, const double* y, double* mine,
                                  double* ref) {
     return guarded([&] {
-        if (fn < 0 || fn > 9 || n < 0 || !x || !mine || !ref || ((fn == 1 || fn == 6 || fn == 7) && !y))
+        if (fn < 0 || fn > 12 || n < 0 || !x || !mine || !ref || ((fn == 1 || fn == 6 || fn == 7 || fn == 12) && !y))
             throw_invalid("math_check: bad arguments");
         if (n > 0) run_math_check(fn, n, x, y, mine, ref);
     });

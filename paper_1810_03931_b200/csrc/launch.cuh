@@ -2,6 +2,8 @@
 // Included by the model translation units (models_*.cu) only.
 #pragma once
 
+#include <atomic>
+
 #include "internal.cuh"
 
 namespace odegpu::detail {
@@ -19,6 +21,8 @@ using dev::guarded_solve_kernel;
 #else
 #define ODEGPU_MB(x) (x)
 #endif
+
+constexpr int kMaxDevices = 64; // occupancy cache slots (per device ordinal)
 
 template <class H>
 struct LaunchPolicy {
@@ -45,11 +49,15 @@ void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
     constexpr std::size_t smem = dev::solve_smem_bytes<H, ALG, kBlock>();
     if constexpr (smem > 48 * 1024) // opt-in above the static limit (per device)
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    static int resident = -1; // per instantiation: resident blocks per SM
-    if (resident < 0) {
+    // resident blocks per SM, per instantiation and device: device threads of
+    // odegpu_solve_pool_multi launch concurrently, and devices may differ
+    static std::atomic<int> resident_of[kMaxDevices] = {};
+    int resident = b->device >= 0 && b->device < kMaxDevices ? resident_of[b->device].load(std::memory_order_relaxed) : 0;
+    if (resident <= 0) {
         int r = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kern, kBlock, smem));
         resident = std::max(r, 1);
+        if (b->device >= 0 && b->device < kMaxDevices) resident_of[b->device].store(resident, std::memory_order_relaxed);
     }
     const Index n = b->a.count;
     const Index persistent = Index(b->num_sms) * resident;

@@ -455,11 +455,16 @@ void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
         }
         for (auto& s : p->slots) s.batch->a.tally = nullptr;
     } catch (...) {
+        // Quiesce every stream of the pipeline before handing control back:
+        // queued D2H copies could otherwise still write into the caller's
+        // page-locked arrays after the error returns, and a later run could
+        // reuse a slot whose old copies are pending.
         for (auto& s : p->slots) s.batch->a.tally = nullptr;
-        for (auto& s : p->slots) {
+        cudaStreamSynchronize(p->copy_in);
+        for (auto& s : p->slots)
             if (s.batch) cudaStreamSynchronize(s.batch->stream);
-            s.busy = false;
-        }
+        cudaStreamSynchronize(p->copy_out);
+        for (auto& s : p->slots) s.busy = false;
         throw;
     }
 }

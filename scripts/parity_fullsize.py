@@ -90,6 +90,22 @@ def main():
         t_ref = time.time() - t0
         g = gpu(wl, its)
         rep = parity.compare(wl, g, ref, **parity.RULES[wl.name])
+        # bitwise: systems whose end state differs in any bit (any array)
+        d = wl.model.dims()
+        n = wl.n
+
+        def differs(a, b, comps):
+            a = np.asarray(a).reshape(comps, n).view(np.uint64)
+            b = np.asarray(b).reshape(comps, n).view(np.uint64)
+            return np.any(a != b, axis=0)
+
+        bit = differs(g["td"], ref["td"], 2) | differs(g["y"], ref["y"], d.system_dim)
+        if d.accessory_count:
+            bit |= differs(g["acc"], ref["acc"], d.accessory_count)
+        og, orf = g["outcomes"], ref["outcomes"]
+        for k in ("final_t", "smallest_step"):
+            bit |= og[k].view(np.uint64) != orf[k].view(np.uint64)
+        rep["bitwise_differing_systems"] = int(bit.sum())
         rep.update(config=name, build=build, n=wl.n, iterations=its, ref_wall_s=round(t_ref, 2),
                    ref_solver_s=round(float(ref["seconds"]), 2), gpu_wall_s=round(g["seconds"], 3))
         # every iteration's integer counts (the end-of-run compare above covers the last)

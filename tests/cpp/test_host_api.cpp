@@ -152,6 +152,46 @@ int main() {
         CHECK(cb.state_at(0, 0) == cb.state_at(1, 0));
     });
 
+    run_case("mutable spans held across solves stay live", [] {
+        // the reference's spans point into live batch storage: a span taken
+        // before solve() shows the solve's results and writes made through it
+        // afterwards reach the next solve (they used to be lost)
+        const auto pool = duffing_pool(4);
+        models::DuffingSystem def;
+        SolverBatch b(make_batch_dims(4, def.dims()));
+        SolverBatch ref(make_batch_dims(4, def.dims()));
+        linear_set(b, pool, {0, 0, 4, CopyMode::All});
+        linear_set(ref, pool, {0, 0, 4, CopyMode::All});
+        auto y = b.state(); // taken once, before any solve
+        auto td = b.time_domain();
+        solve(b, def);
+        solve(ref, def);
+        const SolverBatch& cr = ref;
+        for (Index i = 0; i < 4; ++i) CHECK(y[static_cast<std::size_t>(i)] == cr.state_at(i, 0));
+        // restart system 2 from the origin over [0, 2 pi] through the old spans
+        y[2] = 0.0;
+        y[2 + 4] = 0.0;
+        td[2] = 0.0;
+        td[2 + 4] = kTwoPi;
+        solve(b, def);
+        auto ry = ref.state();
+        auto rtd = ref.time_domain();
+        ry[2] = 0.0;
+        ry[2 + 4] = 0.0;
+        rtd[2] = 0.0;
+        rtd[2 + 4] = kTwoPi;
+        solve(ref, def);
+        ref.detach_spans();
+        b.detach_spans();
+        const SolverBatch& cb = b;
+        const SolverBatch& cr2 = ref;
+        for (Index i = 0; i < 4; ++i) {
+            CHECK(cb.state_at(i, 0) == cr2.state_at(i, 0));
+            CHECK(cb.state_at(i, 1) == cr2.state_at(i, 1));
+        }
+        CHECK(cb.state_at(2, 0) == cb.state_at(2, 0) && cb.outcomes()[2].accepted_steps > 10);
+    });
+
     run_case("random_set permutation identity", [] { // test_batch.cpp:114-139
         const Index n = 64;
         const auto pool = duffing_pool(n);
