@@ -71,6 +71,13 @@ struct BatchArrays {
     // when non-null: each finished system's RK evaluations (trial steps +
     // secant re-steps), the key of the next fetch order
     unsigned* cost = nullptr;
+    // Fused iterations: every system is solved `iterations` times in a row
+    // by the lane that took it up (solve_iteratively without a sink, models
+    // with kFusableIterations); 1 = one solve per launch.
+    int iterations = 1;
+    // When non-null: trial steps (accepted + rejected) of every system and
+    // iteration the launch integrates are added here (one atomic per warp).
+    unsigned long long* trial_steps = nullptr;
     // Scan tallies (ScanDiagnostics, scan.hpp:41-49), accumulated across
     // solves when non-null: [5] detections, [6] detections outside their
     // zone, [7] max |F|/tolerance over detections (bits of a non-negative
@@ -478,7 +485,8 @@ __device__ __forceinline__ Index fetch_system(unsigned long long* work) {
 /// loop; kReadyStep / kReadySecant mean an RK evaluation of length h_step
 /// from (t, y) is pending (a trial step, or one secant re-step).
 enum Phase : int {
-    kFetch = 0, kSetup = 1, kSecant = 2, kCommit = 3, kFinish = 4, kDone = 5, kReadyStep = 6, kReadySecant = 7
+    kFetch = 0, kRefetch = 1, kSetup = 2, kSecant = 3, kCommit = 4, kFinish = 5, kDone = 6, kReadyStep = 7,
+    kReadySecant = 8
 };
 
 constexpr int kMaxSecantIterations = 50; // events.hpp:190
@@ -499,16 +507,31 @@ struct ColdState {
     Real f_land[E][BLOCK];
     Real prev_value[E][BLOCK]; // EventMachine (events.hpp:76-178)
     Real h_try[BLOCK], h_next[BLOCK], t_land[BLOCK];
+    unsigned long long lane_trial_steps[BLOCK]; // lane's trial steps (BatchArrays::trial_steps)
     Real lane_max_ratio[BLOCK];    // lane accumulators for the scan tally,
     unsigned lane_outside[BLOCK];  // over every system the lane integrates
     unsigned lane_not_advanced[BLOCK];
     unsigned lane_detections[BLOCK];
-    Real th_prev[BLOCK], f_prev[BLOCK], th_cur[BLOCK], f_cur[BLOCK], th_min[BLOCK], b_th[BLOCK], b_f[BLOCK];
-    long long sys[BLOCK];
-    unsigned n_det[BLOCK], n_secf[BLOCK];
-    unsigned n_resteps[BLOCK]; // secant re-steps of the current system (its cost beyond the trial steps)
-    int counter[E][BLOCK];
-    int s_it[BLOCK], s_idx[BLOCK], located[BLOCK];
+    // secant iterates (events.hpp:207-240); its lower bound h_try * 1e-12 is
+    // recomputed from h_try (bitwise the same value) instead of stored
+    Real th_prev[BLOCK], f_prev[BLOCK], th_cur[BLOCK], f_cur[BLOCK], b_th[BLOCK], b_f[BLOCK];
+    unsigned sys[BLOCK]; // batch slot (batches hold < 2^32 systems, odegpu_batch_create)
+    // SystemOutcome counters are int64 (driver.hpp:37-40): detections and
+    // secant failures count in 64 bits here; the per-step accepted / rejected
+    // counters (Bookkeeping) count in 32 bits and carry into these high words
+    unsigned long long n_det[BLOCK], n_secf[BLOCK];
+    unsigned acc_hi[BLOCK], rej_hi[BLOCK];
+    // secant re-steps of the current system (its cost beyond the trial steps;
+    // a fetch-order key, saturating) and the fused iterations still to run on
+    // it (BatchArrays::iterations <= 65535 per launch): 16 bits each, so the
+    // Keller-Miksis layout keeps its 5 blocks per SM
+    unsigned short n_resteps[BLOCK], it_left[BLOCK];
+    long long counter[E][BLOCK]; // EventMachine counters (events.hpp:87), Index in the reference
+    // secant iteration (<= kMaxSecantIterations + 1), its event, the located
+    // event (-1: none) and flags: bytes, so that the 64-bit counters above fit
+    // the Keller-Miksis kernel's 5-blocks-per-SM shared-memory budget
+    unsigned char s_it[BLOCK], s_idx[BLOCK];
+    signed char located[BLOCK];
     unsigned char clipped[BLOCK], relocated[BLOCK], s_conv[BLOCK], reason[BLOCK];
     // time-term cache of a time-split model (rk_step): slot s holds the
     // terms at tt_key[s]
@@ -790,6 +813,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
         phase = kCommit;
     };
 
+    ODEGPU_C(lane_trial_steps) = 0ull;
     ODEGPU_C(lane_max_ratio) = 0.0;
     ODEGPU_C(lane_outside) = 0u;
     ODEGPU_C(lane_not_advanced) = 0u;
@@ -798,15 +822,24 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
     for (;;) {
         // ================= PREPARE: bring this lane to a pending RK evaluation
         while (phase < kDone) {
-            if (phase == kFetch) {
-                const Index j = fetch_system(b.work);
-                if (j >= b.count) {
-                    phase = kDone;
-                    break;
+            if (phase <= kRefetch) {
+                // take up a system: the next one of the pool, or (fused
+                // iterations) the same one again from the end point it just
+                // stored — exactly what the next solve() would read
+                Index sys;
+                if (phase == kFetch) {
+                    const Index j = fetch_system(b.work);
+                    if (j >= b.count) {
+                        phase = kDone;
+                        break;
+                    }
+                    sys = b.order ? static_cast<Index>(__ldg(b.order + j)) : j;
+                    if (b.reason[sys] == static_cast<std::uint8_t>(StopReason::NonFiniteAbort)) continue; // solve.hpp:98
+                    ODEGPU_C(it_left) = static_cast<unsigned short>(b.iterations);
+                } else {
+                    sys = static_cast<Index>(ODEGPU_C(sys));
                 }
-                const Index sys = b.order ? static_cast<Index>(__ldg(b.order + j)) : j;
-                if (b.reason[sys] == static_cast<std::uint8_t>(StopReason::NonFiniteAbort)) continue; // solve.hpp:98
-                ODEGPU_C(sys) = sys;
+                ODEGPU_C(sys) = static_cast<unsigned>(sys);
                 if constexpr (kCacheTT) ttc.clear(); // new parameters
                 Real td[2] = {b.td[sys], b.td[sys + n]};
 #pragma unroll
@@ -817,7 +850,9 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
 #pragma unroll
                 for (int i = 0; i < NA; ++i) acc[i] = b.acc[sys + i * n];
                 ODEGPU_B(n_acc) = ODEGPU_B(n_rej) = 0u;
-                ODEGPU_C(n_det) = ODEGPU_C(n_secf) = ODEGPU_C(n_resteps) = 0u;
+                ODEGPU_C(acc_hi) = ODEGPU_C(rej_hi) = 0u;
+                ODEGPU_C(n_det) = ODEGPU_C(n_secf) = 0ull;
+                ODEGPU_C(n_resteps) = 0;
                 ODEGPU_B(smallest) = __longlong_as_double(0x7ff0000000000000LL); // +inf
                 ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::ReachedEndTime);
                 // driver.hpp:96-107
@@ -858,7 +893,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
 #pragma unroll
                 for (int i = 0; i < N; ++i) y[i] = ODEGPU_C(y_land[i]);
                 t = tl;
-                ++ODEGPU_B(n_acc);
+                if (++ODEGPU_B(n_acc) == 0u) ++ODEGPU_C(acc_hi);
                 ODEGPU_B(smallest) = smin(ODEGPU_B(smallest), advanced);
                 bool event_stop = false;
                 Real acc[A];
@@ -866,7 +901,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 if constexpr (E > 0) {
                     const int located = ODEGPU_C(located);
                     bool det[EE];
-                    int cnt[EE];
+                    long long cnt[EE];
 #pragma unroll
                     for (int i = 0; i < E; ++i) { // EventMachine::commit, events.hpp:134-156
                         const int kind = classify(zone_at(ODEGPU_B(zones), i), zone_of(ODEGPU_C(f_land[i]), c.tolerance[i]),
@@ -924,7 +959,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 Real acc[A];
                 load_acc(acc);
                 m.finalize(t, S(td, 2), S(y, N), CS(prow, NP), S(acc, NA));
-                const Index sys = ODEGPU_C(sys);
+                const Index sys = static_cast<Index>(ODEGPU_C(sys));
                 // scan start-time check (src/scan.cpp:296-298): b.td still
                 // holds t0 as fetched
                 if (ODEGPU_C(reason) != static_cast<std::uint8_t>(StopReason::NonFiniteAbort) &&
@@ -938,13 +973,28 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 for (int i = 0; i < NA; ++i) b.acc[sys + i * n] = acc[i];
                 b.final_t[sys] = t;
                 b.reason[sys] = ODEGPU_C(reason);
-                b.accepted[sys] = ODEGPU_B(n_acc);
-                b.rejected[sys] = ODEGPU_B(n_rej);
-                b.detections[sys] = ODEGPU_C(n_det);
-                b.secant_failures[sys] = ODEGPU_C(n_secf);
-                if (b.cost) b.cost[sys] = ODEGPU_B(n_acc) + ODEGPU_B(n_rej) + ODEGPU_C(n_resteps);
+                const Index acc64 = static_cast<Index>((static_cast<unsigned long long>(ODEGPU_C(acc_hi)) << 32) |
+                                                       ODEGPU_B(n_acc));
+                const Index rej64 = static_cast<Index>((static_cast<unsigned long long>(ODEGPU_C(rej_hi)) << 32) |
+                                                       ODEGPU_B(n_rej));
+                b.accepted[sys] = acc64;
+                b.rejected[sys] = rej64;
+                b.detections[sys] = static_cast<Index>(ODEGPU_C(n_det));
+                b.secant_failures[sys] = static_cast<Index>(ODEGPU_C(n_secf));
+                if (b.cost) { // fetch-order key (saturates: only the order of long systems is at stake)
+                    const unsigned long long c64 = static_cast<unsigned long long>(acc64) +
+                                                   static_cast<unsigned long long>(rej64) + ODEGPU_C(n_resteps);
+                    b.cost[sys] = c64 > 0xffffffffull ? 0xffffffffu : static_cast<unsigned>(c64);
+                }
                 b.smallest_step[sys] = ODEGPU_B(smallest);
-                phase = kFetch;
+                ODEGPU_C(lane_trial_steps) += static_cast<unsigned long long>(acc64) + static_cast<unsigned long long>(rej64);
+                // fused iterations: solve the same system again unless it
+                // aborted (a NonFiniteAbort outcome is sticky, solve.hpp:98)
+                const unsigned short left = static_cast<unsigned short>(ODEGPU_C(it_left) - 1);
+                ODEGPU_C(it_left) = left;
+                phase = (left > 0 && ODEGPU_C(reason) != static_cast<std::uint8_t>(StopReason::NonFiniteAbort))
+                            ? kRefetch
+                            : kFetch;
                 continue;
             }
             if (phase == kSecant) {
@@ -964,7 +1014,8 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     end_secant();
                     continue;
                 }
-                theta = sclamp(theta, ODEGPU_C(th_min), ODEGPU_C(h_try));
+                const Real h_try = ODEGPU_C(h_try);
+                theta = sclamp(theta, h_try * 1e-12, h_try); // th_min (events.hpp:209)
                 if (theta == th_cur) {
                     end_secant();
                     continue;
@@ -978,6 +1029,11 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
         // always run once per iteration for all lanes (finished lanes compute
         // on stale state and ignore the result).
         if (__all_sync(0xffffffffu, phase == kDone)) {
+            if (b.trial_steps) {
+                unsigned long long st = ODEGPU_C(lane_trial_steps);
+                for (int o = 16; o > 0; o >>= 1) st += __shfl_xor_sync(0xffffffffu, st, o);
+                if ((threadIdx.x & 31) == 0 && st) atomicAdd(b.trial_steps, st);
+            }
             if (b.tally) { // warp-reduced scan tally, one atomic per counter and warp
                 unsigned outside = ODEGPU_C(lane_outside), not_adv = ODEGPU_C(lane_not_advanced);
                 unsigned dets = ODEGPU_C(lane_detections);
@@ -1051,7 +1107,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     }
                 }
                 if (!accepted) { // driver.hpp:136-140; t < t1 still holds
-                    ++ODEGPU_B(n_rej);
+                    if (++ODEGPU_B(n_rej) == 0u) ++ODEGPU_C(rej_hi);
                     ODEGPU_B(h) = h_next;
                     setup_step(false);
                     continue;
@@ -1092,7 +1148,6 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                         ODEGPU_C(s_conv) = false;
                         ODEGPU_C(th_prev) = 0;
                         ODEGPU_C(th_cur) = h_try;
-                        ODEGPU_C(th_min) = h_try * 1e-12;
                         Real fp = 0, fc = 0;
 #pragma unroll
                         for (int i = 0; i < E; ++i)
@@ -1125,7 +1180,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
 #pragma unroll
             for (int i = 0; i < N; ++i) y[i] = yn[i];
             t = tl;
-            ++ODEGPU_B(n_acc);
+            if (++ODEGPU_B(n_acc) == 0u) ++ODEGPU_C(acc_hi);
             if constexpr (kHasOrdinaryAccessory<H>) {
                 Real acc[A];
                 load_acc(acc);
@@ -1143,7 +1198,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
             else setup_step(false);
         } else if (phase == kReadySecant) { // one secant iteration's step is in (events.hpp:222-240)
             if constexpr (E > 0) {
-                ++ODEGPU_C(n_resteps);
+                if (ODEGPU_C(n_resteps) != 0xffff) ++ODEGPU_C(n_resteps);
                 Real fs[EE];
                 m.event_values(t + h_step, CS(yn, N), CS(prow, NP), S(fs, E));
                 const int s_idx = ODEGPU_C(s_idx);

@@ -80,6 +80,20 @@ concept TimeSplitHooks = DeviceHooks<H> &&
 } && (H::kTimeTermCount > 0);
 // clang-format on
 
+/// Whether consecutive solves of one system may run inside ONE kernel launch
+/// (fused iterations: solve_iteratively without a sink). The reference
+/// checks every system's time domain before each solve (solve.hpp:159-161)
+/// and a batch's trig certificate is computed from the time domains before a
+/// launch, so fusing is exact only when no iteration can leave the checked
+/// time domain: finalize does not write it (the HookDefaults no-op), or the
+/// model declares `static constexpr bool kFinalizeKeepsTimeDomain = true`
+/// (it only moves t0 to the stop time, inside [t0, t1]).
+template <class H>
+inline constexpr bool kFusableIterations = [] {
+    if constexpr (requires { H::kFinalizeKeepsTimeDomain; }) return bool(H::kFinalizeKeepsTimeDomain);
+    else return std::is_same_v<decltype(&H::finalize), decltype(&HookDefaults::finalize)>;
+}();
+
 } // namespace odegpu
 
 #endif

@@ -148,6 +148,7 @@ struct DuffingLyapunovHooks : HookDefaults {
         acc[0] = y[2];
         y[2] = 1.0;
     }
+    static constexpr bool kFinalizeKeepsTimeDomain = true; // finalize never writes td (hooks.hpp)
 };
 
 // ----------------------------------------------------------- host classes

@@ -30,7 +30,16 @@ ODEGPU_HD ODEGPU_INLINE void keller_miksis_time_terms(Real tau, std::span<const 
     const Real arg2 = two_pi * c[11] * tau + c[12];
     Real s1, c1, s2, c2;
     T::sincos(arg1, &s1, &c1);
-    T::sincos(arg2, &s2, &c2);
+    // single-frequency excitation (f2 = f1, theta = 0: the scans' and
+    // BASELINE's bubble pools) gives arg2 == arg1 bit for bit, and sincos is
+    // a function of its argument: reuse the values instead of recomputing
+    // them (bitwise the same terms; the reference evaluates both)
+    if (arg2 == arg1) {
+        s2 = s1;
+        c2 = c1;
+    } else {
+        T::sincos(arg2, &s2, &c2);
+    }
     tt[0] = c[5] * s1 + c[6] * s2;
     tt[1] = c[7] * c1 + c[8] * c2;
 }
@@ -149,6 +158,8 @@ struct BubbleCollapseHooksT : KellerMiksisHooksT<T> {
                             std::span<Real>) const {
         time_domain[0] = t;
     }
+    // finalize moves t0 to the stop time t in [t0, t1] (hooks.hpp)
+    static constexpr bool kFinalizeKeepsTimeDomain = true;
 };
 
 using KellerMiksisHooks = KellerMiksisHooksT<Trig>;

@@ -287,6 +287,7 @@ def _bind(lib):
         "odegpu_batch_launch_count": (C.c_int64, [vp]),
         "odegpu_batch_diagnostics": (C.c_int, [vp, P(Diagnostics)]),
         "odegpu_batch_last_kernel_ms": (C.c_int, [vp, P(C.c_double)]),
+        "odegpu_batch_trial_steps": (C.c_int, [vp, P(Index), C.c_int]),
         "odegpu_batch_trig_certified": (C.c_int, [vp, P(C.c_int)]),
         "odegpu_dfma_peak": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, P(C.c_double), P(C.c_double)]),
         "odegpu_batch_copy": (C.c_int, [vp, vp]),

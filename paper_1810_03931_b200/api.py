@@ -333,6 +333,13 @@ class SolverBatch:
         check(self._lib.odegpu_batch_trig_certified(self._h, C.byref(v)))
         return bool(v.value)
 
+    def trial_steps(self, reset: bool = False) -> int:
+        """Trial steps the batch's solve kernels integrated since creation or
+        the last reset (every system and iteration, fused ones included)."""
+        v = C.c_int64()
+        check(self._lib.odegpu_batch_trial_steps(self._h, C.byref(v), int(reset)))
+        return int(v.value)
+
     def last_kernel_ms(self) -> float:
         v = C.c_double()
         check(self._lib.odegpu_batch_last_kernel_ms(self._h, C.byref(v)))

@@ -135,6 +135,8 @@ size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 odegpu_batch* batch_create(const odegpu_batch_dims& dims, int device) {
     // BatchDims::validate (pool.hpp:67-73)
     if (dims.batch_capacity < 1) throw_invalid("BatchDims: batch_capacity must be >= 1");
+    if (dims.batch_capacity > Index(0xffffffff)) // lanes address slots in 32 bits (solver.cuh ColdState)
+        throw_invalid("BatchDims: batch_capacity must be < 2^32 on the device");
     if (dims.system_dim < 1) throw_invalid("BatchDims: system_dim must be >= 1");
     if (dims.param_count < 0) throw_invalid("BatchDims: param_count must be >= 0");
     if (dims.event_count < 0) throw_invalid("BatchDims: event_count must be >= 0");
@@ -160,7 +162,7 @@ odegpu_batch* batch_create(const odegpu_batch_dims& dims, int device) {
                                 n,                          // reason
                                 n * 8, n * 8, n * 8, n * 8, // counters
                                 n * 8,                      // smallest_step
-                                8, 16, 128};                // work, first_bad + trig flag, diag
+                                8, 16, 128, 8};             // work, first_bad + trig flag, diag, trial steps
         constexpr int kArrays = sizeof(sizes) / sizeof(sizes[0]);
         size_t total = 0;
         for (size_t s : sizes) total += align_up(s);
@@ -186,6 +188,7 @@ odegpu_batch* batch_create(const odegpu_batch_dims& dims, int device) {
         b->a.work = static_cast<unsigned long long*>(ptrs[11]);
         b->first_bad = static_cast<unsigned long long*>(ptrs[12]);
         b->diag = static_cast<unsigned long long*>(ptrs[13]);
+        b->trial_steps = static_cast<unsigned long long*>(ptrs[14]);
         b->a.n = dims.batch_capacity;
         b->a.count = dims.batch_capacity;
         CK(cudaEventCreate(&b->ev_start));
@@ -506,16 +509,28 @@ int odegpu_solve_iteratively(odegpu_batch* b, const odegpu_model* m, const odegp
         const dev::Controls c = prepare_solve(b->dims, m, cfg, ode, ev);
         DeviceGuard g(b->device);
         b->a.count = b->dims.batch_capacity;
+        if (!sink) {
+            // no host round trip between iterations: models whose finalize
+            // keeps the time domain valid run them fused, every system solved
+            // `iterations` times in a row by one lane in as few launches as
+            // possible (hooks.hpp kFusableIterations); the t1 < t0 check of
+            // each launch covers the iterations it fuses
+            for (Index it = 0; it < iterations;) {
+                enqueue_time_check(b);
+                b->fuse_request = iterations - it;
+                launch_model(b, *m, cfg->algorithm, c);
+                it += b->fused_done;
+            }
+            raise_if_bad(b); // a skipped iteration leaves every later one skipped
+            return;
+        }
         for (Index it = 0; it < iterations; ++it) {
             enqueue_time_check(b);
             launch_model(b, *m, cfg->algorithm, c);
-            if (sink) {
-                raise_if_bad(b);
-                sink_rc = sink(it, b, user);
-                if (sink_rc != 0) return;
-            }
+            raise_if_bad(b);
+            sink_rc = sink(it, b, user);
+            if (sink_rc != 0) return;
         }
-        if (!sink) raise_if_bad(b); // a skipped iteration leaves every later one skipped
     });
     return rc != 0 ? rc : sink_rc;
 }
@@ -545,6 +560,19 @@ int odegpu_batch_diagnostics(odegpu_batch* b, odegpu_diagnostics* out) {
         out->secant_failures = static_cast<Index>(h[3]);
         for (int k = 0; k < 4; ++k) out->reason_counts[k] = static_cast<Index>(h[4 + k]);
         out->max_trial_steps = static_cast<Index>(h[8]);
+    });
+}
+
+int odegpu_batch_trial_steps(odegpu_batch* b, odegpu_index* total, int reset) {
+    return guarded([&] {
+        check_batch(b);
+        if (!total) throw_invalid("null argument");
+        DeviceGuard g(b->device);
+        unsigned long long h = 0;
+        CK(cudaMemcpyAsync(&h, b->trial_steps, sizeof h, cudaMemcpyDeviceToHost, b->stream));
+        if (reset) CK(cudaMemsetAsync(b->trial_steps, 0, sizeof h, b->stream));
+        CK(cudaStreamSynchronize(b->stream));
+        *total = static_cast<Index>(h);
     });
 }
 

@@ -96,6 +96,12 @@ struct odegpu_batch {
     unsigned* order = nullptr;
     unsigned* cost = nullptr; // per-system RK evaluations of the last COST-mode solve (BatchArrays::cost)
     bool build_order = true; // false: the next solve's order would go unused (pipeline, last iteration)
+    // fused iterations (solver.cuh BatchArrays::iterations): how many solves
+    // the next launch may run per system, and how many the last one ran
+    // (1 for models whose finalize could invalidate the time domain)
+    odegpu::Index fuse_request = 1;
+    odegpu::Index fused_done = 1;
+    unsigned long long* trial_steps = nullptr; // device: trial steps integrated since the last reset
 };
 
 namespace odegpu::detail {

@@ -80,10 +80,18 @@ void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
     const bool cost = b->order_mode == ODEGPU_FETCH_COST || (b->order_mode == ODEGPU_FETCH_AUTO && kPolicyCost);
     b->a.order = (cost && b->order_count == n) ? b->order : nullptr;
     b->a.cost = (cost && b->build_order) ? b->cost : nullptr; // null until the first order build allocates it
+    // fused iterations: the systems of this launch are solved `fused` times
+    // in a row (hooks.hpp kFusableIterations; one solve otherwise)
+    const Index fused = kFusableIterations<H> ? std::max<Index>(1, std::min<Index>(b->fuse_request, 65535)) : 1;
+    b->a.iterations = static_cast<int>(fused);
+    b->fused_done = fused;
+    b->fuse_request = 1;
+    b->a.trial_steps = b->trial_steps;
     CK(cudaEventRecord(b->ev_start, b->stream));
     kern<<<grid, kBlock, smem, b->stream>>>(hooks, b->a, c, b->first_bad);
     CK(cudaGetLastError());
     CK(cudaEventRecord(b->ev_stop, b->stream));
+    b->a.iterations = 1;
     b->a.order = nullptr;
     const bool have_cost = b->a.cost != nullptr;
     b->a.cost = nullptr;

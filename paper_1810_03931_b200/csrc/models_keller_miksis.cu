@@ -39,6 +39,13 @@ struct LaunchPolicy<models::KellerMiksisHooks> {
     static constexpr bool kCostOrder = true; // step counts spread widely: longest first
 };
 
+// 5 resident blocks need 5 x (layout + 1 KB reserved) <= 228 KB of shared
+// memory per SM: every byte of per-lane cold state counts (solver.cuh
+// ColdState packs its flags and secant indices into bytes for this).
+static_assert(5 * (dev::solve_smem_bytes<models::BubbleCollapseHooks, Algorithm::RKCK45, kBlock>() + 1024) <=
+                  228 * 1024,
+              "Keller-Miksis shared-memory layout no longer fits 5 blocks per SM");
+
 bool family_dims_keller_miksis(const odegpu_model& m, odegpu_system_dims* d) {
     switch (m.id) {
     case ODEGPU_MODEL_KELLER_MIKSIS: set_dims<models::KellerMiksisHooks>(d); return true;

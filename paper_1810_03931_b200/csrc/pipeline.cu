@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -257,14 +258,34 @@ void reserve_records(odegpu_pipeline* p, Index n_rec, uint32_t mask) {
     p->packed.resize(size_t(n_rec * cap));
 }
 
-/// Runs systems [begin, end) of the pool through the pipeline's device.
-void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
+/// Where a pipeline takes its chunks from: consecutive chunks of one range
+/// (a single device), or a queue shared by every device of a multi-GPU run —
+/// each device thread claims the next chunk with fetch_add, the cross-device
+/// analogue of the reference's worker tile claim (solve.hpp:94-95), so fast
+/// devices (or devices that drew cheap systems) take more chunks.
+struct ChunkSource {
+    std::atomic<Index>* shared = nullptr; // multi-device queue (chunk starts), or
+    Index next = 0;                       // the private cursor of a single range
+    Index end = 0;
+    Index step = 0;
+    /// [start, start + count) of the next chunk; false when drained.
+    bool claim(Index cap, Index* start, Index* count) {
+        const Index s = shared ? shared->fetch_add(step) : next;
+        if (!shared) next += step;
+        if (s >= end) return false;
+        *start = s;
+        *count = std::min(cap, end - s);
+        return true;
+    }
+};
+
+/// Runs the chunks `src` hands out through the pipeline's device.
+void run_chunks(odegpu_pipeline* p, const Run& j, ChunkSource& src) {
     const odegpu_pool_dims& pd = j.pool->dims;
     const odegpu_system_dims& sd = p->sd;
     if (sd.system_dim != pd.system_dim || sd.param_count != pd.param_count ||
         sd.accessory_count != pd.accessory_count)
         throw_invalid("solve_pool: definition and pool dimensions disagree");
-    if (end <= begin) return;
     const Index cap = p->cap;
     const odegpu_batch_dims bd{cap, sd.system_dim, sd.param_count, sd.event_count, sd.accessory_count};
     const dev::Controls c = prepare_solve(bd, &p->model, j.cfg, j.ode, j.ev);
@@ -352,12 +373,12 @@ void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
     constexpr int kSlots = odegpu_pipeline::kSlots;
     int k = 0;
     try {
-        for (Index start = begin; start < end; start += cap, ++k) {
+        Index start = 0, n = 0;
+        for (; src.claim(cap, &start, &n); ++k) {
             Slot& s = p->slots[k % kSlots];
             drain(s); // the slot's previous chunk must be consumed before reuse
             odegpu_batch* b = s.batch;
             mark(p->copy_in);
-            const Index n = std::min(cap, end - start);
             s.start = start;
             s.count = n;
             b->a.count = n;
@@ -375,13 +396,20 @@ void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
             CK(cudaStreamWaitEvent(b->stream, s.loaded, 0));
             mark(b->stream);
             launch_reset_outcomes(b, 0, n);
-            for (Index it = 0; it < j.iterations; ++it) {
+            // no per-iteration tally or snapshot to take: the iterations may
+            // run fused in one launch (solve_iteratively without a sink)
+            const bool fuse = !tally && n_rec == 0;
+            for (Index it = 0; it < j.iterations;) {
                 enqueue_time_check(b);
-                b->build_order = it + 1 < j.iterations; // the chunk's last solve: its order would go unused
+                b->fuse_request = fuse ? j.iterations - it : 1;
+                b->build_order = it + b->fuse_request < j.iterations; // the chunk's last solve: order unused
                 launch_model(b, p->model, j.cfg->algorithm, c);
+                const Index done = b->fused_done;
+                it += done;
+                if (done > 1) continue; // fused: no per-iteration work below
                 if (tally) launch_tally(b, tally, false);
-                if (n_rec > 0 && it >= j.record_from) { // snapshots stay ordered with the kernels
-                    const Index r = it - j.record_from;
+                if (n_rec > 0 && it - 1 >= j.record_from) { // snapshots stay ordered with the kernels
+                    const Index r = it - 1 - j.record_from;
                     if (r_td) copy_d2h_strided(s.rec_td + r * 2 * cap, cap, 0, b->a.td, cap, 0, n, 2, b->stream);
                     if (r_y)
                         copy_d2h_strided(s.rec_y + r * sd.system_dim * cap, cap, 0, b->a.state, cap, 0, n,
@@ -467,6 +495,14 @@ void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
         for (auto& s : p->slots) s.busy = false;
         throw;
     }
+}
+
+void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
+    ChunkSource src;
+    src.next = begin;
+    src.end = end;
+    src.step = p->cap;
+    run_chunks(p, j, src);
 }
 
 void validate_run(const odegpu_pool_view* pool, const odegpu_solver_config* cfg, const odegpu_ode_controls* ode,
@@ -598,30 +634,30 @@ int odegpu_solve_pool_multi_tallied(const odegpu_pool_view* pool, const odegpu_p
         std::exception_ptr* failures = new std::exception_ptr[size_t(n_devices)];
         std::vector<std::thread> threads;
         const Index N = pool->dims.problem_size;
-        const Index n_chunks = (N + batch_capacity - 1) / batch_capacity;
+        // one queue of chunks of batch_capacity systems in pool order, shared
+        // by all devices; chunk boundaries do not depend on the device count,
+        // so per-chunk results (and scan rows) equal the single-device run's
+        std::atomic<Index> queue{0};
+        const Index cap = std::min<Index>(batch_capacity, N);
+        (void)chunk_aligned; // chunks are always aligned to batch_capacity now
         for (int d = 0; d < n_devices; ++d) {
-            Index b0 = 0, b1 = 0;
-            if (chunk_aligned) { // whole chunks of batch_capacity per device, in pool order
-                Index c0 = 0, c1 = 0;
-                odegpu_slice(n_chunks, n_devices, d, &c0, &c1);
-                b0 = std::min(N, c0 * batch_capacity);
-                b1 = std::min(N, c1 * batch_capacity);
-            } else {
-                odegpu_slice(N, n_devices, d, &b0, &b1);
-            }
             const Run* jp = &j;
             std::exception_ptr* slot = failures + d;
             const int dev_id = devices[d];
             const odegpu_model m = *model;
-            threads.emplace_back([jp, slot, dev_id, b0, b1, m, batch_capacity] {
+            std::atomic<Index>* q = &queue;
+            threads.emplace_back([jp, slot, dev_id, m, cap, q, N] {
                 odegpu_pipeline* p = nullptr;
                 try {
-                    if (b1 > b0) {
-                        p = pipeline_create(m, std::min<Index>(batch_capacity, b1 - b0), dev_id);
-                        run_range(p, *jp, b0, b1);
-                    }
+                    p = pipeline_create(m, cap, dev_id);
+                    ChunkSource src;
+                    src.shared = q;
+                    src.end = N;
+                    src.step = cap;
+                    run_chunks(p, *jp, src);
                 } catch (...) {
                     *slot = std::current_exception();
+                    q->store(N); // the other devices stop claiming chunks
                 }
                 delete p;
             });

@@ -5,7 +5,8 @@ profiles/<tag>_ncu_summary.md with the counters DESIGN.md argues from: FP64
 pipe activity, issue activity, warps, registers, stall reasons, DRAM bytes,
 local-memory traffic, lane efficiency and the dynamic instruction mix.
 
-    python scripts/ncu_summary.py <tag> [cfg ...]
+    python scripts/ncu_summary.py <tag> [cfg ...]      (reads gpurun_out/<tag>/prof_<cfg>.ncu-rep,
+                                                         else gpurun_out/prof_<cfg>.ncu-rep)
 """
 import csv
 import io
@@ -18,7 +19,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 NAMES = {"cfg1": "cfg1_duffing_rk4", "cfg2": "cfg2_duffing_rkck45_event", "cfg3": "cfg3_keller_miksis",
-         "cfg4": "cfg4_valve"}
+         "cfg4": "cfg4_valve", "cfg5": "cfg5_keller_miksis_2^24"}
 METRICS = {
     "duration_ms": ("gpu__time_duration.sum", 1e-6),
     "fp64_pipe_active_pct": ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", 1),
@@ -86,10 +87,13 @@ def main():
     summary.setdefault("traffic_bytes_per_launch", {})
     summary.setdefault("kernels", {})
     lines = [f"# ncu summary ({tag})", "",
-             "One `ncu --set full` capture of the solve kernel per workload (full BASELINE size, "
-             "second solve of the process; ncu clocks/replay make durations longer than the bench's).", ""]
+             "One `ncu --set full --clock-control none` capture of the solve kernel per workload (full "
+             "BASELINE size, in the bench's step shape: cfg2 from the initial conditions, the others the 4th "
+             "in-place iteration; scripts/gpu_ncu_r02.sh). Durations are of a kernel timed alone under replay.", ""]
     for c in cfgs:
-        rep = ROOT / "gpurun_out" / f"prof_{c}.ncu-rep"
+        rep = ROOT / "gpurun_out" / tag / f"prof_{c}.ncu-rep"
+        if not rep.exists():
+            rep = ROOT / "gpurun_out" / f"prof_{c}.ncu-rep"
         if not rep.exists():
             continue
         m = raw_metrics(rep)
