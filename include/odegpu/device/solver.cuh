@@ -45,6 +45,10 @@ struct Controls {
     Real tolerance[kMaxEvents];
     Index stop_condition[kMaxEvents];
     int direction[kMaxEvents];
+    // classify_transition per event as a table: 2 bits (kind + 1) for each
+    // (previous zone, next zone) pair, built from `direction` on the host
+    // (controls_from), so the per-step peek is a shift and a mask
+    unsigned kind_lut[kMaxEvents];
     Index max_steps_in_zone;
 };
 
@@ -445,15 +449,18 @@ __device__ __forceinline__ bool rk_step(const H& m, Real t, Real h, const Real (
 enum : int { kZoneBelow = 0, kZoneInside = 1, kZoneAbove = 2, kZoneNone = 3 };
 enum : int { kKindNone = -1, kKindAcross = 0, kKindEntered = 1 };
 
+/// events.hpp:22-33, as selects: it runs on every accepted step.
 __device__ __forceinline__ int zone_of(Real v, Real tol) {
-    if (!isfinite(v)) return kZoneNone;
-    if (fabs(v) <= tol) return kZoneInside;
-    return v > 0 ? kZoneAbove : kZoneBelow;
+    const bool fin = fabs(v) < __longlong_as_double(0x7ff0000000000000LL); // false for inf and NaN
+    int z = v > 0 ? kZoneAbove : kZoneBelow;
+    z = fabs(v) <= tol ? kZoneInside : z;
+    return fin ? z : kZoneNone;
 }
 
 /// classify_transition (events.hpp:54-70) from the previous zone; kZoneNone
 /// on either side and Inside before (phase Leaving) give no detection.
-__device__ __forceinline__ int classify(int prev, int next, int direction) {
+/// (Host and device: controls_from tabulates it per event direction.)
+__host__ __device__ constexpr int classify(int prev, int next, int direction) {
     if (prev == kZoneAbove && direction <= 0) {
         if (next == kZoneBelow) return kKindAcross;
         if (next == kZoneInside) return kKindEntered;
@@ -463,6 +470,18 @@ __device__ __forceinline__ int classify(int prev, int next, int direction) {
         if (next == kZoneInside) return kKindEntered;
     }
     return kKindNone;
+}
+
+/// classify() looked up in the event's table (Controls::kind_lut).
+__device__ __forceinline__ int classify_lut(int prev, int next, unsigned lut) {
+    return static_cast<int>((lut >> (2 * (4 * prev + next))) & 3u) - 1;
+}
+__host__ __device__ constexpr unsigned kind_table(int direction) {
+    unsigned lut = 0;
+    for (int prev = 0; prev < 4; ++prev)
+        for (int next = 0; next < 4; ++next)
+            lut |= static_cast<unsigned>(classify(prev, next, direction) + 1) << (2 * (4 * prev + next));
+    return lut;
 }
 
 __device__ __forceinline__ int zone_at(int zones, int i) { return (zones >> (2 * i)) & 3; }
@@ -797,6 +816,20 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
         }
         ODEGPU_B(steps_in_zone) = any_inside ? ODEGPU_B(steps_in_zone) + 1 : 0;
     };
+    // refresh() given the zones of fp already computed.
+    const auto refresh_zones = [&](const Real (&fp)[EE], const int (&zn)[EE]) {
+        bool any_inside = false;
+        int zones = ODEGPU_B(zones);
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+            const bool keep = zn[i] == kZoneNone; // non-finite: keep the previous arming
+            if (!keep) ODEGPU_C(prev_value[i]) = fp[i];
+            zones = keep ? zones : with_zone(zones, i, zn[i]);
+            any_inside = any_inside || zn[i] == kZoneInside;
+        }
+        ODEGPU_B(zones) = zones;
+        ODEGPU_B(steps_in_zone) = any_inside ? ODEGPU_B(steps_in_zone) + 1 : 0;
+    };
     // Ends a secant location (driver.hpp:157-164).
     const auto end_secant = [&]() {
         if (!ODEGPU_C(s_conv)) ++ODEGPU_C(n_secf);
@@ -812,6 +845,39 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
         for (int i = 0; i < E; ++i) ODEGPU_C(f_land[i]) = f[i];
         phase = kCommit;
     };
+
+    // One secant iteration's pre-step exits (events.hpp:214-219): the next
+    // re-step length (kReadySecant), or the end of the location (kCommit).
+    const auto secant_step = [&]() {
+        if (ODEGPU_C(s_it) > kMaxSecantIterations) {
+            end_secant();
+            return;
+        }
+        const Real th_cur = ODEGPU_C(th_cur), f_cur = ODEGPU_C(f_cur);
+        const Real denom = f_cur - ODEGPU_C(f_prev);
+        if (denom == 0) {
+            end_secant();
+            return;
+        }
+        Real theta = th_cur - f_cur * (th_cur - ODEGPU_C(th_prev)) / denom;
+        if (!isfinite(theta)) {
+            end_secant();
+            return;
+        }
+        const Real h_try = ODEGPU_C(h_try);
+        theta = sclamp(theta, h_try * 1e-12, h_try); // th_min (events.hpp:209)
+        if (theta == th_cur) {
+            end_secant();
+            return;
+        }
+        h_step = theta;
+        phase = kReadySecant;
+    };
+#if ODEGPU_SECANT_INLINE
+#define ODEGPU_SECANT_NEXT() secant_step()
+#else
+#define ODEGPU_SECANT_NEXT() (phase = kSecant)
+#endif
 
     ODEGPU_C(lane_trial_steps) = 0ull;
     ODEGPU_C(lane_max_ratio) = 0.0;
@@ -904,8 +970,8 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     long long cnt[EE];
 #pragma unroll
                     for (int i = 0; i < E; ++i) { // EventMachine::commit, events.hpp:134-156
-                        const int kind = classify(zone_at(ODEGPU_B(zones), i), zone_of(ODEGPU_C(f_land[i]), c.tolerance[i]),
-                                                  c.direction[i]);
+                        const int kind = classify_lut(zone_at(ODEGPU_B(zones), i),
+                                                      zone_of(ODEGPU_C(f_land[i]), c.tolerance[i]), c.kind_lut[i]);
                         det[i] = kind != kKindNone || i == located;
                         cnt[i] = ODEGPU_C(counter[i]) + (det[i] ? 1 : 0);
                         ODEGPU_C(counter[i]) = cnt[i];
@@ -998,30 +1064,8 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 continue;
             }
             if (phase == kSecant) {
-                // events.hpp:214-219: the pre-step exits of one secant iteration
-                if (ODEGPU_C(s_it) > kMaxSecantIterations) {
-                    end_secant();
-                    continue;
-                }
-                const Real th_cur = ODEGPU_C(th_cur), f_cur = ODEGPU_C(f_cur);
-                const Real denom = f_cur - ODEGPU_C(f_prev);
-                if (denom == 0) {
-                    end_secant();
-                    continue;
-                }
-                Real theta = th_cur - f_cur * (th_cur - ODEGPU_C(th_prev)) / denom;
-                if (!isfinite(theta)) {
-                    end_secant();
-                    continue;
-                }
-                const Real h_try = ODEGPU_C(h_try);
-                theta = sclamp(theta, h_try * 1e-12, h_try); // th_min (events.hpp:209)
-                if (theta == th_cur) {
-                    end_secant();
-                    continue;
-                }
-                h_step = theta;
-                phase = kReadySecant;
+                secant_step();
+                continue;
             }
         }
         // Warp-uniform exit: every lane stays resident until its whole warp
@@ -1120,14 +1164,14 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 m.event_values(tl, CS(yn, N), CS(prow, NP), S(f, E));
                 // EventMachine::peek (events.hpp:111-125): highest index wins
                 int located = -1, kind = kKindNone;
+                int zn[EE]; // the landed zones, also what refresh() stores
 #pragma unroll
-                for (int i = E - 1; i >= 0; --i) {
-                    if (located >= 0) break;
-                    const int k = classify(zone_at(ODEGPU_B(zones), i), zone_of(f[i], c.tolerance[i]), c.direction[i]);
-                    if (k != kKindNone) {
-                        located = i;
-                        kind = k;
-                    }
+                for (int i = 0; i < E; ++i) zn[i] = zone_of(f[i], c.tolerance[i]);
+#pragma unroll
+                for (int i = 0; i < E; ++i) { // ascending: the highest index wins
+                    const int k = classify_lut(zone_at(ODEGPU_B(zones), i), zn[i], c.kind_lut[i]);
+                    located = k != kKindNone ? i : located;
+                    kind = k != kKindNone ? k : kind;
                 }
                 if (located >= 0) { // detection: the slow path through PREPARE
                     ODEGPU_C(t_land) = tl;
@@ -1159,7 +1203,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                         ODEGPU_C(f_cur) = fc;
                         ODEGPU_C(b_th) = h_try;
                         ODEGPU_C(b_f) = fc;
-                        phase = kSecant;
+                        ODEGPU_SECANT_NEXT();
                     }
                     continue;
                 }
@@ -1168,7 +1212,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                     phase = kFinish;
                     continue;
                 }
-                refresh(f); // no detection: commit records nothing, f_post = f_landed
+                refresh_zones(f, zn); // no detection: commit records nothing, f_post = f_landed
             } else {
                 if (tl <= t) {
                     ODEGPU_C(reason) = static_cast<std::uint8_t>(StopReason::NonFiniteAbort);
@@ -1230,12 +1274,13 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 ODEGPU_C(th_cur) = h_step;
                 ODEGPU_C(f_cur) = f;
                 ++ODEGPU_C(s_it);
-                phase = kSecant;
+                ODEGPU_SECANT_NEXT();
             }
         }
     }
 #undef ODEGPU_C
 #undef ODEGPU_B
+#undef ODEGPU_SECANT_NEXT
 }
 
 /// A model whose hooks have a CertifiedTrig twin (include/odegpu/trig.hpp).
@@ -1299,6 +1344,7 @@ inline Controls controls_from(const odegpu_system_dims& sys, const odegpu_solver
     c.max_steps_in_zone = ev ? ev->max_steps_in_zone : 50;
     for (Index i = 0; i < sys.event_count; ++i) {
         c.direction[i] = ev->direction[i];
+        c.kind_lut[i] = kind_table(ev->direction[i]);
         c.tolerance[i] = ev->tolerance[i];
         c.stop_condition[i] = ev->stop_condition[i];
     }
