@@ -87,6 +87,22 @@ struct BatchArrays {
     // zone, [7] max |F|/tolerance over detections (bits of a non-negative
     // double), [8] systems whose t0 did not advance over the solve (kTally*).
     unsigned long long* tally = nullptr;
+    // Per-detection log (the reference's on_detection observer,
+    // solve.hpp:46-50 / driver.hpp:186-206), when non-null: one record per
+    // committed detection, appended at slot atomicAdd(log_count, 1) while
+    // slots last (later ones are only counted). SoA columns of log_capacity.
+    unsigned long long* log_count = nullptr;
+    Index log_capacity = 0;
+    unsigned* log_system = nullptr;          // batch index
+    int* log_event = nullptr;                // event index
+    int* log_kind = nullptr;                 // DetectionKind (events.hpp:31)
+    int* log_in_zone = nullptr;
+    long long* log_counter = nullptr;        // Detection::counter (1-based)
+    long long* log_sequence = nullptr;       // the system's detection number in this solve
+    Real* log_t = nullptr;
+    Real* log_value = nullptr;
+    Real* log_y_pre = nullptr;               // [dim][capacity]: state before event_action
+    Real* log_y_post = nullptr;              // [dim][capacity]: state after it
 };
 
 /// Slots of the scan tally (shared with the tally kernel, csrc/kernels.cu).
@@ -726,7 +742,7 @@ constexpr std::size_t solve_smem_bytes() {
 /// the next step's clipping — so a lane is ready for its next evaluation
 /// without another trip through the state machine. Only detections, stops
 /// and system ends go back through PREPARE.
-template <class H, Algorithm ALG, int BLOCK, class Pol = EffectivePolicy<H>>
+template <class H, Algorithm ALG, int BLOCK, class Pol = EffectivePolicy<H>, bool LOG = false>
 __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, const Controls& c) {
     constexpr int N = H::kSystemDim;
     constexpr int NP = H::kParamCount, NA = H::kAccessoryCount, E = H::kEventCount;
@@ -844,6 +860,41 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
 #pragma unroll
         for (int i = 0; i < E; ++i) ODEGPU_C(f_land[i]) = f[i];
         phase = kCommit;
+    };
+
+    // Appends the detection records of a commit (BatchArrays::log_*): the
+    // events in `mask`, classified against the zones before the commit,
+    // counters and landed values from the cold state, y_land before and y
+    // after the event action. Everything it reads lives in the cold state,
+    // so the commit path keeps no extra registers for it.
+    const auto log_detections = [&](const BatchArrays& bb, const Controls& cc, int zones_before, unsigned mask) {
+        long long seq = static_cast<long long>(ODEGPU_C(n_det)) - __popc(mask); // n_det already counts them
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+            if (!(mask >> i & 1u)) continue;
+            const unsigned long long slot = atomicAdd(bb.log_count, 1ull);
+            const long long q = seq++;
+            if (slot >= static_cast<unsigned long long>(bb.log_capacity)) continue;
+            const Index r = static_cast<Index>(slot);
+            const Real v = ODEGPU_C(f_land[i]);
+            const int prev = zone_at(zones_before, i);
+            const int kn = classify_lut(prev, zone_of(v, cc.tolerance[i]), cc.kind_lut[i]);
+            bb.log_system[r] = ODEGPU_C(sys);
+            bb.log_event[r] = i;
+            // SteppedAcross, EnteredFromAbove, EnteredFromBelow (events.hpp:31); a
+            // forced (located, no longer classified) detection is SteppedAcross
+            bb.log_kind[r] = kn == kKindEntered ? (prev == kZoneAbove ? 1 : 2) : 0;
+            bb.log_in_zone[r] = isfinite(v) && fabs(v) <= cc.tolerance[i];
+            bb.log_counter[r] = ODEGPU_C(counter[i]);
+            bb.log_sequence[r] = q;
+            bb.log_t[r] = t;
+            bb.log_value[r] = v;
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                bb.log_y_pre[r + j * bb.log_capacity] = ODEGPU_C(y_land[j]);
+                bb.log_y_post[r + j * bb.log_capacity] = y[j];
+            }
+        }
     };
 
     // One secant iteration's pre-step exits (events.hpp:214-219): the next
@@ -987,6 +1038,9 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                             ODEGPU_C(lane_max_ratio) = smax(ODEGPU_C(lane_max_ratio), ratio);
                         }
                     }
+                    // the zones the detections were classified against (refresh()
+                    // re-arms them below): the detection log's kinds
+                    const int zones_before = ODEGPU_B(zones);
                     Real f_post[EE];
                     if (located >= 0) {
 #pragma unroll
@@ -1001,6 +1055,12 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
 #pragma unroll
                     for (int i = 0; i < E; ++i)
                         if (det[i]) m.event_accessory(i, cnt[i], t, CS(y, N), CS(prow, NP), S(acc, NA));
+                    if constexpr (LOG) { // the records, in event order (driver.hpp:204-206)
+                        unsigned mask = 0;
+#pragma unroll
+                        for (int i = 0; i < E; ++i) mask |= det[i] ? 1u << i : 0u;
+                        log_detections(b, c, zones_before, mask);
+                    }
 #pragma unroll
                     for (int i = 0; i < E; ++i)
                         if (det[i] && c.stop_condition[i] != 0 && cnt[i] >= c.stop_condition[i]) event_stop = true;
@@ -1312,19 +1372,24 @@ __global__ void trig_certificate_kernel(BatchArrays b, unsigned long long* flags
 /// trig certificate: the model's certified_hooks instantiation (no range
 /// branch in its trig) runs instead of the general one; both share one
 /// shared-memory layout and policy.
-template <class H, Algorithm ALG, int BLOCK, int MIN_BLOCKS>
+///
+/// LOG: the instantiation that also records every detection (BatchArrays
+/// log_*, the reference's on_detection observer), launched only while a
+/// batch has a detection log — like the reference's `observing` branch
+/// (driver.hpp:186-206) it costs nothing when nobody observes.
+template <class H, Algorithm ALG, int BLOCK, int MIN_BLOCKS, bool LOG = false>
 __global__ void __launch_bounds__(BLOCK, MIN_BLOCKS)
     guarded_solve_kernel(H model, BatchArrays b, Controls c, const unsigned long long* flags) {
     if (flags[0] != ~0ull) return;
     dmath::init_shared_tables();
     if constexpr (TrigCertifiable<H>) {
         if (flags[1] == 0) {
-            solve_lanes<typename H::certified_hooks, ALG, BLOCK, EffectivePolicy<H>>(typename H::certified_hooks{},
-                                                                                   b, c);
+            solve_lanes<typename H::certified_hooks, ALG, BLOCK, EffectivePolicy<H>, LOG>(
+                typename H::certified_hooks{}, b, c);
             return;
         }
     }
-    solve_lanes<H, ALG, BLOCK, EffectivePolicy<H>>(model, b, c);
+    solve_lanes<H, ALG, BLOCK, EffectivePolicy<H>, LOG>(model, b, c);
 }
 
 /// Kernel controls from the C-ABI structs (materialised once per solve,

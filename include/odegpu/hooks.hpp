@@ -94,6 +94,20 @@ inline constexpr bool kFusableIterations = [] {
     else return std::is_same_v<decltype(&H::finalize), decltype(&HookDefaults::finalize)>;
 }();
 
+/// Whether a solve leaves every system's time domain exactly as it found it:
+/// neither initialize nor finalize writes it (the HookDefaults no-ops), or
+/// the model declares `static constexpr bool kTimeDomainUnchanged = true`
+/// (hooks that override initialize / finalize without touching the time
+/// domain). The chunked pipeline then does not copy time domains back to a
+/// host pool they were read from (pipeline.cu).
+template <class H>
+inline constexpr bool kKeepsTimeDomain = [] {
+    if constexpr (requires { H::kTimeDomainUnchanged; }) return bool(H::kTimeDomainUnchanged);
+    else
+        return std::is_same_v<decltype(&H::initialize), decltype(&HookDefaults::initialize)> &&
+               std::is_same_v<decltype(&H::finalize), decltype(&HookDefaults::finalize)>;
+}();
+
 } // namespace odegpu
 
 #endif

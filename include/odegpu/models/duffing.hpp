@@ -63,6 +63,7 @@ struct DuffingHooksT : HookDefaults {
 /// DuffingMaxAccessorySystem (duffing.hpp:92-117): running max of y1 + time.
 template <class T = Trig>
 struct DuffingMaxAccessoryHooksT : DuffingHooksT<T> {
+    static constexpr bool kTimeDomainUnchanged = true; // initialize writes state / accessories only
     static constexpr Index kAccessoryCount = 2;
     using certified_hooks = DuffingMaxAccessoryHooksT<CertifiedTrig>;
     ODEGPU_HD void initialize(Real t, std::span<Real>, std::span<Real> y, std::span<const Real>,
@@ -83,6 +84,7 @@ struct DuffingMaxAccessoryHooksT : DuffingHooksT<T> {
 /// local maxima of y1; the event accessory keeps the largest and its time.
 template <class T = Trig>
 struct DuffingMaxEventHooksT : DuffingHooksT<T> {
+    static constexpr bool kTimeDomainUnchanged = true; // initialize writes state / accessories only
     static constexpr Index kEventCount = 1, kAccessoryCount = 2;
     using certified_hooks = DuffingMaxEventHooksT<CertifiedTrig>;
     ODEGPU_HD void event_values(Real, std::span<const Real> y, std::span<const Real>, std::span<Real> f) const {
@@ -106,6 +108,7 @@ struct DuffingMaxEventHooksT : DuffingHooksT<T> {
 /// their times, acc = [y1_max, t_max, y1_min, t_min], seeded at t0.
 template <class T = Trig>
 struct DuffingMaxMinHooksT : DuffingHooksT<T> {
+    static constexpr bool kTimeDomainUnchanged = true; // initialize writes state / accessories only
     static constexpr Index kAccessoryCount = 4;
     using certified_hooks = DuffingMaxMinHooksT<CertifiedTrig>;
     ODEGPU_HD void initialize(Real t, std::span<Real>, std::span<Real> y, std::span<const Real>,
@@ -149,6 +152,7 @@ struct DuffingLyapunovHooks : HookDefaults {
         y[2] = 1.0;
     }
     static constexpr bool kFinalizeKeepsTimeDomain = true; // finalize never writes td (hooks.hpp)
+    static constexpr bool kTimeDomainUnchanged = true;
 };
 
 // ----------------------------------------------------------- host classes

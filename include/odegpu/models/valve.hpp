@@ -33,6 +33,7 @@ ODEGPU_HD ODEGPU_INLINE void valve_impact_action(Index event_index, Real, std::s
 /// ValveSystem (valve.hpp:64-103): F0 = y2 (stop at the next maximum),
 /// F1 = y1 (impact action, continue); acc = running max/min of y1.
 struct ValveHooks : HookDefaults {
+    static constexpr bool kTimeDomainUnchanged = true; // initialize writes accessories only
     static constexpr Index kSystemDim = 3, kParamCount = 5, kEventCount = 2, kAccessoryCount = 2;
     ODEGPU_HD void ode_rhs(Real t, std::span<const Real> y, std::span<const Real> p, std::span<Real> dy) const {
         valve_rhs(t, y, p, dy);

@@ -4,13 +4,19 @@
 //
 // Validation and its messages are the reference's (performed in libodegpu);
 // failures are rethrown as std::invalid_argument / std::out_of_range.
-// solve() is synchronous like the reference. Host observers are not
-// supported on the device; per-solve tallies come from
-// SolverBatch diagnostics instead.
+// solve() is synchronous like the reference. Of the host observers
+// (SolveObservers, solve.hpp:36-50) the detection observer is supported:
+// the device records every detection in a log and on_detection runs on the
+// calling thread after the solve, per system in the order the driver made
+// them (the reference runs it on worker threads, systems interleaved). A
+// per-step observer cannot run on the device: passing one
+// is a compile error; per-solve tallies come from SolverBatch diagnostics.
 #ifndef ODEGPU_SOLVE_HPP
 #define ODEGPU_SOLVE_HPP
 
+#include <cstdint>
 #include <exception>
+#include <span>
 #include <type_traits>
 #include <stdexcept>
 #include <utility>
@@ -21,6 +27,32 @@
 #include "odegpu/system.hpp"
 
 namespace odegpu {
+
+/// How a detection step met the zone (events.hpp:28-31).
+enum class DetectionKind : std::uint8_t { SteppedAcross, EnteredFromAbove, EnteredFromBelow };
+
+/// One recorded event detection (events.hpp:36-47).
+struct Detection {
+    Index event_index = 0;
+    DetectionKind kind = DetectionKind::SteppedAcross;
+    Real t = 0;
+    Real value = 0;
+    Index counter = 0;
+    bool in_zone = false;
+};
+
+/// Observer no-ops and bundle (solve.hpp:36-50).
+struct NoBatchStepObserver {
+    void operator()(Index, Real, std::span<const Real>) const {}
+};
+struct NoBatchDetectionObserver {
+    void operator()(Index, const Detection&, std::span<const Real>, std::span<const Real>) const {}
+};
+template <typename StepObs = NoBatchStepObserver, typename DetObs = NoBatchDetectionObserver>
+struct SolveObservers {
+    StepObs on_step{};
+    DetObs on_detection{};
+};
 
 namespace detail {
 
@@ -110,6 +142,62 @@ struct NoSink {
 
 } // namespace detail
 
+namespace detail {
+
+template <typename StepObs, typename DetObs>
+constexpr bool kObservesDetections = !std::is_same_v<std::remove_cvref_t<DetObs>, NoBatchDetectionObserver>;
+
+template <typename StepObs>
+constexpr void require_no_step_observer() {
+    static_assert(std::is_same_v<std::remove_cvref_t<StepObs>, NoBatchStepObserver>,
+                  "odegpu: a per-step observer (on_step) cannot run on the device; use SolverBatch diagnostics");
+}
+
+/// Runs `solve_one` with the batch's detection log enabled, then hands each
+/// record to on_detection in (system, sequence) order. The log starts at 4
+/// records per system; a solve that detects more is repeated from a device
+/// copy of its inputs with a log large enough (results are deterministic).
+template <typename DetObs, typename SolveOne>
+void with_detection_log(SolverBatch& batch, DetObs& on_detection, SolveOne&& solve_one) {
+    const Index dim = batch.dims().system_dim;
+    Index cap = 4 * batch.size();
+    odegpu_index count = 0, total = 0;
+    batch.push();
+    const auto dd = batch.dims();
+    const odegpu_batch_dims bd{dd.batch_capacity, dd.system_dim, dd.param_count, dd.event_count, dd.accessory_count};
+    odegpu_batch* before = nullptr;
+    check(odegpu_batch_create(&bd, odegpu_batch_device(batch.handle()), &before));
+    struct Release {
+        odegpu_batch* b;
+        ~Release() { odegpu_batch_destroy(b); }
+    } release{before};
+    check(odegpu_batch_copy(before, batch.handle()));
+    check(odegpu_batch_set_detection_log(batch.handle(), cap));
+    solve_one();
+    check(odegpu_batch_read_detection_log(batch.handle(), nullptr, nullptr, nullptr, 0, &count, &total));
+    if (total > cap) { // overflowed: the same inputs again, with room for every record
+        cap = total;
+        check(odegpu_batch_copy(batch.handle(), before));
+        check(odegpu_batch_set_detection_log(batch.handle(), cap));
+        solve_one();
+    }
+    std::vector<odegpu_detection> rec(static_cast<std::size_t>(total));
+    std::vector<Real> pre(static_cast<std::size_t>(total * dim)), post(static_cast<std::size_t>(total * dim));
+    const int rc = odegpu_batch_read_detection_log(batch.handle(), rec.data(), pre.data(), post.data(), total, &count,
+                                                   &total);
+    check(odegpu_batch_set_detection_log(batch.handle(), 0));
+    check(rc);
+    for (odegpu_index k = 0; k < count; ++k) {
+        const odegpu_detection& r = rec[static_cast<std::size_t>(k)];
+        const Detection d{r.event_index, static_cast<DetectionKind>(r.kind), r.t, r.value, r.counter, r.in_zone != 0};
+        on_detection(static_cast<Index>(r.system), d,
+                     std::span<const Real>(pre.data() + k * dim, static_cast<std::size_t>(dim)),
+                     std::span<const Real>(post.data() + k * dim, static_cast<std::size_t>(dim)));
+    }
+}
+
+} // namespace detail
+
 /// Integrates every system of the batch on the GPU (solve.hpp:60-128).
 /// Built-in models run through the C ABI; other SystemModels through a
 /// kernel instantiated from include/odegpu/device/custom.cuh.
@@ -119,6 +207,20 @@ void solve(SolverBatch& batch, const D& def, const SolverConfig& cfg = {}) {
         detail::solve_builtin(batch, def, cfg);
     else
         solve_custom(batch, def, cfg);
+}
+
+/// solve() with observers (solve.hpp:60-63): on_detection receives every
+/// detection of the solve (see the file comment for the order).
+template <SystemModel D, typename StepObs, typename DetObs>
+void solve(SolverBatch& batch, const D& def, const SolverConfig& cfg, SolveObservers<StepObs, DetObs> observers) {
+    detail::require_no_step_observer<StepObs>();
+    if constexpr (!detail::kObservesDetections<StepObs, DetObs> || !BuiltinModel<D>) {
+        static_assert(!detail::kObservesDetections<StepObs, DetObs> || BuiltinModel<D>,
+                      "odegpu: the detection log is available for the built-in models");
+        solve(batch, def, cfg);
+    } else {
+        detail::with_detection_log(batch, observers.on_detection, [&] { detail::solve_builtin(batch, def, cfg); });
+    }
 }
 
 /// solve.hpp:133-142: `iterations` solves, sink(i, const batch&) after each.
@@ -133,6 +235,18 @@ void solve_iteratively(SolverBatch& batch, const D& def, const SolverConfig& cfg
             solve_custom(batch, def, cfg);
             sink(i, static_cast<const SolverBatch&>(batch));
         }
+    }
+}
+
+/// solve_iteratively with observers (solve.hpp:133-142): every iteration's
+/// detections go to on_detection before that iteration's sink.
+template <SystemModel D, typename Sink, typename StepObs, typename DetObs>
+void solve_iteratively(SolverBatch& batch, const D& def, const SolverConfig& cfg, Index iterations, Sink&& sink,
+                       SolveObservers<StepObs, DetObs> observers) {
+    if (iterations < 1) throw std::invalid_argument("solve_iteratively: iterations must be >= 1");
+    for (Index i = 0; i < iterations; ++i) {
+        solve(batch, def, cfg, observers);
+        sink(i, static_cast<const SolverBatch&>(batch));
     }
 }
 

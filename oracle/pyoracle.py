@@ -112,6 +112,29 @@ def solve(which: str, model, td, y, p, acc, *, algorithm: int, dt: float, iterat
     return outcomes, secs.value, tr
 
 
+def reference_detections(wl, iterations: int = 1, workers: int = 4):
+    """Run the reference (oracle/_ref) on a workload with its own
+    on_detection observer attached (solve.hpp:46-50): the last solve's
+    detections as (records [abi.DETECTION_DTYPE], y_pre, y_post) in
+    (system, call) order, plus the solve's result dict."""
+    lib = load("reference")
+    lib.odref_capture_detections.argtypes = [C.c_int]
+    lib.odref_detections.restype = abi.Index
+    lib.odref_detections.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, abi.Index]
+    lib.odref_capture_detections(1)
+    try:
+        res = solve_workload("reference", wl, iterations, workers=workers)
+        total = lib.odref_detections(None, None, None, 0)
+        dim = wl.model.dims().system_dim
+        rec = np.zeros(total, dtype=abi.DETECTION_DTYPE)
+        pre, post = np.zeros((total, dim)), np.zeros((total, dim))
+        if total:
+            lib.odref_detections(abi.vptr(rec), abi.vptr(pre), abi.vptr(post), total)
+    finally:
+        lib.odref_capture_detections(0)
+    return rec, pre, post, res
+
+
 def solve_workload(which: str, wl, iterations: int | None = None, trace: bool = False, workers: int = 1):
     td, y, p, acc = wl.arrays()
     oc, secs, tr = solve(which, wl.model, td, y, p, acc, algorithm=wl.algorithm, dt=wl.dt,

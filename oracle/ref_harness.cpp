@@ -155,6 +155,18 @@ struct Trace {
     odegpu_outcome* outcomes;
 };
 
+// Detection capture (odref_capture_detections): the reference's own
+// on_detection observer (solve.hpp:46-50) records every detection of the
+// LAST solve of a run, per system in call order.
+struct RefDetection {
+    Index event_index, counter;
+    double t, value;
+    int kind, in_zone;
+    std::vector<double> y_pre, y_post;
+};
+bool g_capture = false;
+std::vector<std::vector<RefDetection>> g_dets;
+
 template <SystemModel D>
 int run(const D& def, Index n, double* td, double* y, const double* p, double* acc, odegpu_outcome* outcomes,
         int keep_outcomes, const SolverConfig& cfg, Index iterations, const Trace* trace, double* seconds) {
@@ -171,7 +183,16 @@ int run(const D& def, Index n, double* td, double* y, const double* p, double* a
         std::memcpy(static_cast<void*>(batch.outcomes().data()), outcomes, sizeof(odegpu_outcome) * n);
 
     const auto t0 = std::chrono::steady_clock::now();
-    solve_iteratively(batch, def, cfg, iterations, [&](Index it, const SolverBatch& b) {
+    if (g_capture) g_dets.assign(static_cast<std::size_t>(n), {});
+    auto on_detection = [](Index s, const Detection& d, std::span<const Real> pre, std::span<const Real> post) {
+        // workers own disjoint systems: one vector per system needs no lock
+        g_dets[static_cast<std::size_t>(s)].push_back(RefDetection{d.event_index, d.counter, d.t, d.value,
+                                                                   static_cast<int>(d.kind), d.in_zone ? 1 : 0,
+                                                                   {pre.begin(), pre.end()},
+                                                                   {post.begin(), post.end()}});
+    };
+    auto sink = [&](Index it, const SolverBatch& b) {
+        if (g_capture && it + 1 < iterations) g_dets.assign(static_cast<std::size_t>(n), {}); // keep the last solve's
         if (!trace) return;
         const auto off = static_cast<std::size_t>(it);
         if (trace->td) std::copy(b.time_domain().begin(), b.time_domain().end(), trace->td + off * 2 * n);
@@ -182,7 +203,12 @@ int run(const D& def, Index n, double* td, double* y, const double* p, double* a
         if (trace->outcomes)
             std::memcpy(static_cast<void*>(trace->outcomes + off * n), b.outcomes().data(),
                         sizeof(odegpu_outcome) * n);
-    });
+    };
+    if (g_capture)
+        solve_iteratively(batch, def, cfg, iterations, sink,
+                          SolveObservers<NoBatchStepObserver, decltype(on_detection)>{{}, on_detection});
+    else
+        solve_iteratively(batch, def, cfg, iterations, sink);
     const auto t1 = std::chrono::steady_clock::now();
     if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
 
@@ -216,6 +242,34 @@ T with_ode(Index dim, const odegpu_ode_controls* c) {
 extern "C" {
 
 const char* odref_last_error(void) { return g_err.c_str(); }
+
+// Turns the detection capture of odref_solve on (1) or off (0).
+void odref_capture_detections(int on) {
+    g_capture = on != 0;
+    if (!g_capture) g_dets.clear();
+}
+
+// The captured detections of the last odref_solve in (system, call) order,
+// in the C ABI's record layout (odegpu_detection) with system_dim doubles
+// each of y_pre / y_post; returns the number available, writes <= capacity.
+odegpu_index odref_detections(odegpu_detection* out, double* y_pre, double* y_post, odegpu_index capacity) {
+    odegpu_index k = 0, total = 0;
+    for (std::size_t s = 0; s < g_dets.size(); ++s) {
+        for (std::size_t q = 0; q < g_dets[s].size(); ++q, ++total) {
+            if (k >= capacity || !out) continue;
+            const RefDetection& d = g_dets[s][q];
+            out[k] = odegpu_detection{static_cast<odegpu_index>(s), d.event_index, d.counter,
+                                      static_cast<odegpu_index>(q), d.t, d.value, d.kind, d.in_zone};
+            const std::size_t dim = d.y_pre.size();
+            for (std::size_t j = 0; j < dim; ++j) {
+                if (y_pre) y_pre[static_cast<std::size_t>(k) * dim + j] = d.y_pre[j];
+                if (y_post) y_post[static_cast<std::size_t>(k) * dim + j] = d.y_post[j];
+            }
+            ++k;
+        }
+    }
+    return total;
+}
 
 // Runs `iterations` reference solves over n systems held in SoA arrays
 // (td, y, acc updated in place; outcomes written). keep_outcomes != 0 seeds

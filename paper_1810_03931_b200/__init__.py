@@ -8,6 +8,7 @@ from . import abi, models, scan, workloads  # noqa: F401
 from .api import (  # noqa: F401
     BatchDims,
     CopyMode,
+    DevicePool,
     InvalidArgument,
     LinearCopySpec,
     OdegpuError,
@@ -20,8 +21,10 @@ from .api import (  # noqa: F401
     dfma_peak,
     flat_index,
     linear_set,
+    linear_set_device,
     make_batch_dims,
     random_set,
+    random_set_device,
     solve,
     solve_iteratively,
     batch_copy,

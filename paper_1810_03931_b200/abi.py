@@ -129,6 +129,18 @@ class EventControls(C.Structure):
     ]
 
 
+# odegpu_detection: one record of the detection log (the reference's
+# on_detection observer: Detection, events.hpp:40-47), 56 bytes.
+DETECTION_DTYPE = np.dtype(
+    {
+        "names": ["system", "event_index", "counter", "sequence", "t", "value", "kind", "in_zone"],
+        "formats": ["<i8", "<i8", "<i8", "<i8", "<f8", "<f8", "<i4", "<i4"],
+        "offsets": [0, 8, 16, 24, 32, 40, 48, 52],
+        "itemsize": 56,
+    }
+)
+DETECTION_KINDS = ("SteppedAcross", "EnteredFromAbove", "EnteredFromBelow")  # events.hpp:31
+
 # odegpu_outcome / odensemble::SystemOutcome (driver.hpp:34-42), 56 bytes.
 OUTCOME_DTYPE = np.dtype(
     {
@@ -285,6 +297,21 @@ def _bind(lib):
         ),
         "odegpu_batch_sync": (C.c_int, [vp]),
         "odegpu_batch_launch_count": (C.c_int64, [vp]),
+        "odegpu_batch_set_detection_log": (C.c_int, [vp, Index]),
+        "odegpu_batch_device": (C.c_int, [vp]),
+        "odegpu_device_pool_create": (C.c_int, [P(PoolDims), C.c_int, P(vp)]),
+        "odegpu_device_pool_destroy": (None, [vp]),
+        "odegpu_device_pool_write": (C.c_int, [vp, C.c_int32, Index, Index, P(C.c_double), Index]),
+        "odegpu_device_pool_read": (C.c_int, [vp, C.c_int32, Index, Index, P(C.c_double), Index]),
+        "odegpu_device_pool_read_outcomes": (C.c_int, [vp, Index, Index, vp]),
+        "odegpu_linear_set_device": (C.c_int, [vp, vp, P(LinearCopySpec)]),
+        "odegpu_random_set_device": (C.c_int, [vp, vp, P(Index), P(Index), Index, C.c_int32]),
+        "odegpu_device_pool_store": (C.c_int, [vp, vp, P(Index), P(Index), Index, C.c_int32]),
+        "odegpu_device_pool_solve": (C.c_int, [vp, P(Model), P(SolverConfig), P(OdeControls), P(EventControls),
+                                               Index, Index, C.c_int32]),
+        "odegpu_model_keeps_time_domain": (C.c_int, [P(Model), P(C.c_int)]),
+        "odegpu_batch_read_detection_log": (C.c_int, [vp, vp, P(C.c_double), P(C.c_double), Index, P(Index),
+                                                      P(Index)]),
         "odegpu_batch_diagnostics": (C.c_int, [vp, P(Diagnostics)]),
         "odegpu_batch_last_kernel_ms": (C.c_int, [vp, P(C.c_double)]),
         "odegpu_batch_trial_steps": (C.c_int, [vp, P(Index), C.c_int]),

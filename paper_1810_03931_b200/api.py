@@ -319,6 +319,29 @@ class SolverBatch:
     def launch_count(self) -> int:
         return int(self._lib.odegpu_batch_launch_count(self._h))
 
+    def set_detection_log(self, capacity: int):
+        """Record every detection of the following solves (the reference's
+        on_detection observer, solve.hpp:46-50); 0 disables the log."""
+        check(self._lib.odegpu_batch_set_detection_log(self._h, int(capacity)))
+
+    def detection_log(self, capacity: int | None = None):
+        """The last solve's detections ordered by (system, sequence):
+        (records [abi.DETECTION_DTYPE], y_pre [k, dim], y_post [k, dim], total)."""
+        dim = self.dims.system_dim
+        cnt, tot = C.c_int64(), C.c_int64()
+        check(self._lib.odegpu_batch_read_detection_log(self._h, None, None, None, 0, C.byref(cnt), C.byref(tot)))
+        k = min(int(tot.value), capacity if capacity is not None else int(tot.value))
+        rec = np.zeros(k, dtype=abi.DETECTION_DTYPE)
+        pre = np.zeros((k, dim))
+        post = np.zeros((k, dim))
+        if k:
+            dp = C.POINTER(C.c_double)
+            check(self._lib.odegpu_batch_read_detection_log(self._h, rec.ctypes.data_as(C.c_void_p),
+                                                            pre.ctypes.data_as(dp), post.ctypes.data_as(dp),
+                                                            k, C.byref(cnt), C.byref(tot)))
+            rec, pre, post = rec[: cnt.value], pre[: cnt.value], post[: cnt.value]
+        return rec, pre, post, int(tot.value)
+
     def diagnostics(self) -> dict:
         """Device-side tally of the last solve's outcomes."""
         d = abi.Diagnostics()
@@ -361,6 +384,119 @@ def random_set(batch: SolverBatch, pool: ProblemPool, spec: RandomCopySpec):
     P = C.POINTER(C.c_int64)
     check(batch._lib.odegpu_random_set(batch.handle, C.byref(pool.view()), ib.ctypes.data_as(P),
                                        ip.ctypes.data_as(P), ib.size, spec.copy_mode))
+
+
+class DevicePool:
+    """A ProblemPool (pool.hpp:12-64) kept in HBM (odegpu_device_pool_*):
+    linear_set / random_set from it are device gathers; solve() runs the
+    whole pool in chunks, cost-clustered on request."""
+
+    def __init__(self, dims: PoolDims, device: int = 0):
+        dims.validate()
+        self._lib = abi.load()
+        self.dims = dims
+        self.device = device
+        h = C.c_void_p()
+        check(self._lib.odegpu_device_pool_create(C.byref(abi.PoolDims(dims.problem_size, dims.system_dim,
+                                                                         dims.param_count, dims.accessory_count)),
+                                                  device, C.byref(h)))
+        self._h = h
+
+    @classmethod
+    def from_pool(cls, pool: ProblemPool, device: int = 0) -> "DevicePool":
+        dp = cls(pool.dims, device)
+        dp.upload(pool)
+        return dp
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.odegpu_device_pool_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _comps(self, prop):
+        d = self.dims
+        return {abi.PROP_TIME_DOMAIN: 2, abi.PROP_STATE: d.system_dim, abi.PROP_PARAMETERS: d.param_count,
+                abi.PROP_ACCESSORIES: d.accessory_count}[prop]
+
+    def write(self, prop: int, a: np.ndarray, start: int = 0, count: int | None = None):
+        n = self.dims.problem_size if count is None else count
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        if a.size != self._comps(prop) * n:
+            raise InvalidArgument("device pool: array size != components x count")
+        check(self._lib.odegpu_device_pool_write(self._h, prop, start, n, abi.dptr(a if a.size else None), n))
+
+    def read(self, prop: int, start: int = 0, count: int | None = None) -> np.ndarray:
+        n = self.dims.problem_size if count is None else count
+        out = np.zeros(self._comps(prop) * n)
+        check(self._lib.odegpu_device_pool_read(self._h, prop, start, n, abi.dptr(out if out.size else None), n))
+        return out
+
+    def upload(self, pool: ProblemPool):
+        for prop, a in ((abi.PROP_TIME_DOMAIN, pool.time_domain()), (abi.PROP_STATE, pool.state()),
+                        (abi.PROP_PARAMETERS, pool.parameters()), (abi.PROP_ACCESSORIES, pool.accessories())):
+            if a.size:
+                self.write(prop, a)
+
+    def time_domain(self):
+        return self.read(abi.PROP_TIME_DOMAIN)
+
+    def state(self):
+        return self.read(abi.PROP_STATE)
+
+    def parameters(self):
+        return self.read(abi.PROP_PARAMETERS)
+
+    def accessories(self):
+        return self.read(abi.PROP_ACCESSORIES)
+
+    def outcomes(self) -> np.ndarray:
+        o = np.zeros(self.dims.problem_size, dtype=abi.OUTCOME_DTYPE)
+        check(self._lib.odegpu_device_pool_read_outcomes(self._h, 0, o.size, abi.vptr(o)))
+        return o
+
+    def solve(self, defn: SystemDef, cfg: SolverConfig | None = None, batch_capacity: int | None = None,
+              iterations: int = 1, clustered: bool = True):
+        """odegpu_device_pool_solve: every system `iterations` times in place."""
+        m, c, ode, ev, _ = _prepared(defn, cfg or SolverConfig())
+        cap = batch_capacity or self.dims.problem_size
+        check(self._lib.odegpu_device_pool_solve(self._h, m, c, ode, ev, cap, iterations, int(bool(clustered))))
+
+    def store(self, batch: SolverBatch, spec: RandomCopySpec):
+        """Batch slots spec.indices_in_batch back into pool rows spec.indices_in_pool."""
+        ib = np.ascontiguousarray(spec.indices_in_batch, dtype=np.int64)
+        ip = np.ascontiguousarray(spec.indices_in_pool, dtype=np.int64)
+        if ib.size != ip.size:
+            raise InvalidArgument("store: index lists differ in length")
+        Pt = C.POINTER(C.c_int64)
+        check(self._lib.odegpu_device_pool_store(self._h, batch.handle, ib.ctypes.data_as(Pt), ip.ctypes.data_as(Pt),
+                                                 ib.size, spec.copy_mode))
+
+
+def linear_set_device(batch: SolverBatch, pool: DevicePool, spec: LinearCopySpec):
+    """batch.cpp:78-104 from a device pool."""
+    c = abi.LinearCopySpec(spec.start_in_batch, spec.start_in_pool, spec.element_count, spec.copy_mode, 0)
+    check(batch._lib.odegpu_linear_set_device(batch.handle, pool.handle, C.byref(c)))
+
+
+def random_set_device(batch: SolverBatch, pool: DevicePool, spec: RandomCopySpec):
+    """batch.cpp:106-135 from a device pool."""
+    ib = np.ascontiguousarray(spec.indices_in_batch, dtype=np.int64)
+    ip = np.ascontiguousarray(spec.indices_in_pool, dtype=np.int64)
+    if ib.size != ip.size:
+        raise InvalidArgument("random_set: index lists differ in length")
+    Pt = C.POINTER(C.c_int64)
+    check(batch._lib.odegpu_random_set_device(batch.handle, pool.handle, ib.ctypes.data_as(Pt),
+                                              ip.ctypes.data_as(Pt), ib.size, spec.copy_mode))
 
 
 def _controls(defn: SystemDef):

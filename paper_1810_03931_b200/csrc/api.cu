@@ -68,6 +68,15 @@ odegpu_system_dims dims_of(const odegpu_model& m) {
     throw_unsupported("unknown model id " + std::to_string(m.id));
 }
 
+bool keeps_time_domain(const odegpu_model& m) {
+    odegpu_system_dims d{};
+    bool keeps = false;
+    if (family_dims_duffing(m, &d, &keeps) || family_dims_keller_miksis(m, &d, &keeps) ||
+        family_dims_valve(m, &d, &keeps) || family_dims_fakes(m, &d, &keeps))
+        return keeps;
+    throw_unsupported("unknown model id " + std::to_string(m.id));
+}
+
 void launch_model(odegpu_batch* b, const odegpu_model& m, int algorithm, const dev::Controls& c) {
     if (family_launch_duffing(b, m, algorithm, c) || family_launch_keller_miksis(b, m, algorithm, c) ||
         family_launch_valve(b, m, algorithm, c) || family_launch_fakes(b, m, algorithm, c))
@@ -253,6 +262,7 @@ void odegpu_batch_destroy(odegpu_batch* b) {
     if (b->stream) cudaStreamSynchronize(b->stream);
     if (b->block) cudaFree(b->block);
     if (b->order_block) cudaFree(b->order_block);
+    if (b->log_block) cudaFree(b->log_block);
     if (b->host_flag) cudaFreeHost(b->host_flag);
     if (b->ev_start) cudaEventDestroy(b->ev_start);
     if (b->ev_stop) cudaEventDestroy(b->ev_stop);
@@ -543,7 +553,120 @@ int odegpu_batch_sync(odegpu_batch* b) {
     });
 }
 
+int odegpu_batch_set_detection_log(odegpu_batch* b, odegpu_index capacity) {
+    return guarded([&] {
+        check_batch(b);
+        if (capacity < 0) throw_invalid("detection log: capacity must be >= 0");
+        DeviceGuard g(b->device);
+        CK(cudaStreamSynchronize(b->stream));
+        if (b->log_block) CK(cudaFree(b->log_block));
+        b->log_block = nullptr;
+        auto& a = b->a;
+        a.log_count = nullptr;
+        a.log_capacity = 0;
+        if (capacity == 0) return;
+        const size_t c = size_t(capacity), dim = size_t(b->dims.system_dim);
+        const size_t sizes[] = {8, c * 4, c * 4, c * 4, c * 4, c * 8, c * 8, c * 8, c * 8, dim * c * 8, dim * c * 8};
+        size_t total = 0;
+        for (size_t v : sizes) total += align_up(v);
+        CK(cudaMalloc(&b->log_block, total));
+        char* q = static_cast<char*>(b->log_block);
+        void* ptr[11];
+        for (int i = 0; i < 11; ++i) {
+            ptr[i] = q;
+            q += align_up(sizes[i]);
+        }
+        a.log_count = static_cast<unsigned long long*>(ptr[0]);
+        a.log_system = static_cast<unsigned*>(ptr[1]);
+        a.log_event = static_cast<int*>(ptr[2]);
+        a.log_kind = static_cast<int*>(ptr[3]);
+        a.log_in_zone = static_cast<int*>(ptr[4]);
+        a.log_counter = static_cast<long long*>(ptr[5]);
+        a.log_sequence = static_cast<long long*>(ptr[6]);
+        a.log_t = static_cast<Real*>(ptr[7]);
+        a.log_value = static_cast<Real*>(ptr[8]);
+        a.log_y_pre = static_cast<Real*>(ptr[9]);
+        a.log_y_post = static_cast<Real*>(ptr[10]);
+        a.log_capacity = capacity;
+        CK(cudaMemsetAsync(a.log_count, 0, 8, b->stream));
+    });
+}
+
+int odegpu_batch_read_detection_log(odegpu_batch* b, odegpu_detection* records, double* y_pre, double* y_post,
+                                    odegpu_index capacity, odegpu_index* count, odegpu_index* total) {
+    return guarded([&] {
+        check_batch(b);
+        if (!count || !total) throw_invalid("null argument");
+        const auto& a = b->a;
+        if (!a.log_count) throw_invalid("detection log: not enabled (odegpu_batch_set_detection_log)");
+        DeviceGuard g(b->device);
+        unsigned long long n_all = 0;
+        CK(cudaMemcpyAsync(&n_all, a.log_count, 8, cudaMemcpyDeviceToHost, b->stream));
+        CK(cudaStreamSynchronize(b->stream));
+        const Index stored = std::min<Index>(static_cast<Index>(n_all), a.log_capacity);
+        *total = static_cast<Index>(n_all);
+        const Index n = std::min<Index>(stored, std::max<Index>(capacity, 0));
+        *count = 0;
+        if (n == 0) return;
+        if (!records) throw_invalid("null argument");
+        const size_t c = size_t(stored), dim = size_t(b->dims.system_dim);
+        std::vector<unsigned> sys(c);
+        std::vector<int> ev(c), kind(c), zone(c);
+        std::vector<long long> cnt(c), seq(c);
+        std::vector<Real> t(c), v(c), pre(dim * c), post(dim * c);
+        auto get = [&](void* dst, const void* src, size_t bytes) {
+            CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, b->stream));
+        };
+        get(sys.data(), a.log_system, c * 4);
+        get(ev.data(), a.log_event, c * 4);
+        get(kind.data(), a.log_kind, c * 4);
+        get(zone.data(), a.log_in_zone, c * 4);
+        get(cnt.data(), a.log_counter, c * 8);
+        get(seq.data(), a.log_sequence, c * 8);
+        get(t.data(), a.log_t, c * 8);
+        get(v.data(), a.log_value, c * 8);
+        for (size_t j = 0; j < dim; ++j) {
+            get(pre.data() + j * c, a.log_y_pre + j * size_t(a.log_capacity), c * 8);
+            get(post.data() + j * c, a.log_y_post + j * size_t(a.log_capacity), c * 8);
+        }
+        CK(cudaStreamSynchronize(b->stream));
+        // slots are claimed in completion order across lanes: hand records
+        // out per system in the order its driver made them
+        std::vector<size_t> idx(c);
+        for (size_t i = 0; i < c; ++i) idx[i] = i;
+        std::sort(idx.begin(), idx.end(), [&](size_t x, size_t y) {
+            return sys[x] != sys[y] ? sys[x] < sys[y] : seq[x] < seq[y];
+        });
+        for (Index k = 0; k < n; ++k) {
+            const size_t i = idx[size_t(k)];
+            odegpu_detection& d = records[k];
+            d.system = sys[i];
+            d.event_index = ev[i];
+            d.counter = cnt[i];
+            d.sequence = seq[i];
+            d.t = t[i];
+            d.value = v[i];
+            d.kind = kind[i];
+            d.in_zone = zone[i];
+            for (size_t j = 0; j < dim; ++j) {
+                if (y_pre) y_pre[size_t(k) * dim + j] = pre[j * c + i];
+                if (y_post) y_post[size_t(k) * dim + j] = post[j * c + i];
+            }
+        }
+        *count = n;
+    });
+}
+
 int64_t odegpu_batch_launch_count(const odegpu_batch* b) { return b ? b->launches : 0; }
+
+int odegpu_batch_device(const odegpu_batch* b) { return b ? b->device : -1; }
+
+int odegpu_model_keeps_time_domain(const odegpu_model* m, int* keeps) {
+    return guarded([&] {
+        if (!m || !keeps) throw_invalid("null argument");
+        *keeps = keeps_time_domain(*m) ? 1 : 0;
+    });
+}
 
 int odegpu_batch_diagnostics(odegpu_batch* b, odegpu_diagnostics* out) {
     return guarded([&] {

@@ -45,19 +45,27 @@ void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
         else return detail::kBlock;
 #endif
     }();
-    auto kern = guarded_solve_kernel<H, ALG, kBlock, kMin>;
+    // the detection-log instantiation only for models with events, and only
+    // while the batch has a log (odegpu_batch_set_detection_log); its own
+    // launch bounds leave it one block per SM fewer (more registers for the
+    // observer path instead of spills)
+    const bool log = H::kEventCount > 0 && b->a.log_count != nullptr;
+    auto kern = guarded_solve_kernel<H, ALG, kBlock, kMin, false>;
+    if constexpr (H::kEventCount > 0)
+        if (log) kern = guarded_solve_kernel<H, ALG, kBlock, (kMin > 1 ? kMin - 1 : 1), true>;
     constexpr std::size_t smem = dev::solve_smem_bytes<H, ALG, kBlock>();
     if constexpr (smem > 48 * 1024) // opt-in above the static limit (per device)
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     // resident blocks per SM, per instantiation and device: device threads of
     // odegpu_solve_pool_multi launch concurrently, and devices may differ
-    static std::atomic<int> resident_of[kMaxDevices] = {};
-    int resident = b->device >= 0 && b->device < kMaxDevices ? resident_of[b->device].load(std::memory_order_relaxed) : 0;
+    static std::atomic<int> resident_of[2][kMaxDevices] = {};
+    auto& cache = resident_of[log ? 1 : 0];
+    int resident = b->device >= 0 && b->device < kMaxDevices ? cache[b->device].load(std::memory_order_relaxed) : 0;
     if (resident <= 0) {
         int r = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kern, kBlock, smem));
         resident = std::max(r, 1);
-        if (b->device >= 0 && b->device < kMaxDevices) resident_of[b->device].store(resident, std::memory_order_relaxed);
+        if (b->device >= 0 && b->device < kMaxDevices) cache[b->device].store(resident, std::memory_order_relaxed);
     }
     const Index n = b->a.count;
     const Index persistent = Index(b->num_sms) * resident;
@@ -82,7 +90,11 @@ void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
     b->a.cost = (cost && b->build_order) ? b->cost : nullptr; // null until the first order build allocates it
     // fused iterations: the systems of this launch are solved `fused` times
     // in a row (hooks.hpp kFusableIterations; one solve otherwise)
-    const Index fused = kFusableIterations<H> ? std::max<Index>(1, std::min<Index>(b->fuse_request, 65535)) : 1;
+    // (not with a detection log: its records belong to one solve)
+    const Index fused = kFusableIterations<H> && !b->a.log_count
+                            ? std::max<Index>(1, std::min<Index>(b->fuse_request, 65535))
+                            : 1;
+    if (b->a.log_count) CK(cudaMemsetAsync(b->a.log_count, 0, sizeof(unsigned long long), b->stream));
     b->a.iterations = static_cast<int>(fused);
     b->fused_done = fused;
     b->fuse_request = 1;
@@ -109,8 +121,9 @@ void launch_alg(odegpu_batch* b, const H& hooks, int algorithm, const dev::Contr
 }
 
 template <class H>
-void set_dims(odegpu_system_dims* d) {
+void set_dims(odegpu_system_dims* d, bool* keeps_time_domain = nullptr) {
     *d = odegpu_system_dims{H::kSystemDim, H::kParamCount, H::kEventCount, H::kAccessoryCount};
+    if (keeps_time_domain) *keeps_time_domain = kKeepsTimeDomain<H>;
 }
 
 } // namespace odegpu::detail

@@ -49,13 +49,13 @@ struct LaunchPolicy<models::DuffingLyapunovHooks> {
     static constexpr bool kCostOrder = true;
 };
 
-bool family_dims_duffing(const odegpu_model& m, odegpu_system_dims* d) {
+bool family_dims_duffing(const odegpu_model& m, odegpu_system_dims* d, bool* keeps) {
     switch (m.id) {
-    case ODEGPU_MODEL_DUFFING: set_dims<models::DuffingHooks>(d); return true;
-    case ODEGPU_MODEL_DUFFING_MAX_ACCESSORY: set_dims<models::DuffingMaxAccessoryHooks>(d); return true;
-    case ODEGPU_MODEL_DUFFING_MAX_EVENT: set_dims<models::DuffingMaxEventHooks>(d); return true;
-    case ODEGPU_MODEL_DUFFING_MAXMIN: set_dims<models::DuffingMaxMinHooks>(d); return true;
-    case ODEGPU_MODEL_DUFFING_LYAPUNOV: set_dims<models::DuffingLyapunovHooks>(d); return true;
+    case ODEGPU_MODEL_DUFFING: set_dims<models::DuffingHooks>(d, keeps); return true;
+    case ODEGPU_MODEL_DUFFING_MAX_ACCESSORY: set_dims<models::DuffingMaxAccessoryHooks>(d, keeps); return true;
+    case ODEGPU_MODEL_DUFFING_MAX_EVENT: set_dims<models::DuffingMaxEventHooks>(d, keeps); return true;
+    case ODEGPU_MODEL_DUFFING_MAXMIN: set_dims<models::DuffingMaxMinHooks>(d, keeps); return true;
+    case ODEGPU_MODEL_DUFFING_LYAPUNOV: set_dims<models::DuffingLyapunovHooks>(d, keeps); return true;
     default: return false;
     }
 }

@@ -22,18 +22,18 @@ struct KernelPolicy<fakes::RampHooks> {
 
 namespace odegpu::detail {
 
-bool family_dims_fakes(const odegpu_model& m, odegpu_system_dims* d) {
+bool family_dims_fakes(const odegpu_model& m, odegpu_system_dims* d, bool* keeps) {
     switch (m.id) {
-    case ODEGPU_MODEL_CONSTANT: set_dims<fakes::ConstantHooks>(d); return true;
-    case ODEGPU_MODEL_CUBIC_TIME: set_dims<fakes::CubicTimeHooks>(d); return true;
-    case ODEGPU_MODEL_EXPONENTIAL: set_dims<fakes::ExponentialHooks>(d); return true;
-    case ODEGPU_MODEL_UNIT_SLOPE: set_dims<fakes::UnitSlopeHooks>(d); return true;
-    case ODEGPU_MODEL_COUNTING: set_dims<fakes::CountingHooks>(d); return true;
-    case ODEGPU_MODEL_RAMP: set_dims<fakes::RampHooks>(d); return true;
-    case ODEGPU_MODEL_DECAY: set_dims<fakes::DecayHooks>(d); return true;
-    case ODEGPU_MODEL_SEAT_CONTACT: set_dims<fakes::SeatContactHooks>(d); return true;
-    case ODEGPU_MODEL_HARMONIC: set_dims<fakes::HarmonicHooks>(d); return true;
-    case ODEGPU_MODEL_BLOWUP: set_dims<fakes::BlowUpHooks>(d); return true;
+    case ODEGPU_MODEL_CONSTANT: set_dims<fakes::ConstantHooks>(d, keeps); return true;
+    case ODEGPU_MODEL_CUBIC_TIME: set_dims<fakes::CubicTimeHooks>(d, keeps); return true;
+    case ODEGPU_MODEL_EXPONENTIAL: set_dims<fakes::ExponentialHooks>(d, keeps); return true;
+    case ODEGPU_MODEL_UNIT_SLOPE: set_dims<fakes::UnitSlopeHooks>(d, keeps); return true;
+    case ODEGPU_MODEL_COUNTING: set_dims<fakes::CountingHooks>(d, keeps); return true;
+    case ODEGPU_MODEL_RAMP: set_dims<fakes::RampHooks>(d, keeps); return true;
+    case ODEGPU_MODEL_DECAY: set_dims<fakes::DecayHooks>(d, keeps); return true;
+    case ODEGPU_MODEL_SEAT_CONTACT: set_dims<fakes::SeatContactHooks>(d, keeps); return true;
+    case ODEGPU_MODEL_HARMONIC: set_dims<fakes::HarmonicHooks>(d, keeps); return true;
+    case ODEGPU_MODEL_BLOWUP: set_dims<fakes::BlowUpHooks>(d, keeps); return true;
     default: return false;
     }
 }

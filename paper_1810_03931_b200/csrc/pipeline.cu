@@ -311,6 +311,9 @@ void run_chunks(odegpu_pipeline* p, const Run& j, ChunkSource& src) {
     // page-locked (async D2H, no host copy), else via pinned staging.
     const odegpu_pool_out none{};
     const odegpu_pool_out& o = j.out ? *j.out : none;
+    // Time domains a solve cannot change (hooks.hpp kKeepsTimeDomain) need
+    // no copy back into the pool array they were read from (in-place runs).
+    const bool td_back = o.time_domain && !(o.time_domain == j.pool->time_domain && keeps_time_domain(p->model));
     const bool d_td = is_pinned(o.time_domain), d_y = is_pinned(o.state),
                d_acc = sd.accessory_count && is_pinned(o.accessories), d_out = is_pinned(o.outcomes);
 
@@ -326,7 +329,7 @@ void run_chunks(odegpu_pipeline* p, const Run& j, ChunkSource& src) {
         auto put = [&](double* dst, const double* src, Index comps) {
             for (Index cc = 0; cc < comps; ++cc) std::memcpy(dst + off + cc * N, src + cc * cap, size_t(n) * 8);
         };
-        if (o.time_domain && !d_td) put(o.time_domain, s.fin_td, 2);
+        if (td_back && !d_td) put(o.time_domain, s.fin_td, 2);
         if (o.state && !d_y) put(o.state, s.fin_y, sd.system_dim);
         if (o.accessories && sd.accessory_count && !d_acc) put(o.accessories, s.fin_acc, sd.accessory_count);
         if (o.outcomes && !d_out) std::memcpy(o.outcomes + off, s.fin_out, size_t(n) * sizeof(odegpu_outcome));
@@ -392,8 +395,16 @@ void run_chunks(odegpu_pipeline* p, const Run& j, ChunkSource& src) {
             if (sd.accessory_count)
                 copy_h2d_strided(b->a.acc, cap, 0, j.pool->accessories, N, start, n, sd.accessory_count, p->copy_in);
             CK(cudaEventRecord(s.loaded, p->copy_in));
-            // kernels: fresh outcomes, then every iteration back to back
+            // kernels: fresh outcomes, then every iteration back to back.
+            // At most two chunks compute at once: chunk k starts once chunk
+            // k-2's kernels are done, so chunk k-1 has the device to itself
+            // but for chunk k filling its tail. (With every in-flight chunk
+            // computing at once they all finished together, late: their D2H,
+            // and so the next chunks' H2D into the freed slots, came in
+            // bursts that left the device idle between them — 4-chunk groups
+            // in the ODEGPU_PIPELINE_TRACE timeline of the 2^24 pool.)
             CK(cudaStreamWaitEvent(b->stream, s.loaded, 0));
+            if (k >= 2) CK(cudaStreamWaitEvent(b->stream, p->slots[(k - 2) % kSlots].computed, 0));
             mark(b->stream);
             launch_reset_outcomes(b, 0, n);
             // no per-iteration tally or snapshot to take: the iterations may
@@ -426,12 +437,13 @@ void run_chunks(odegpu_pipeline* p, const Run& j, ChunkSource& src) {
                 CK(cudaGetLastError());
                 ++b->launches;
             }
+            mark(b->stream);
             CK(cudaEventRecord(s.computed, b->stream));
             // endpoints on the copy-out stream
             CK(cudaStreamWaitEvent(p->copy_out, s.computed, 0));
             mark(p->copy_out);
             cudaStream_t out_s = p->copy_out;
-            if (o.time_domain) {
+            if (td_back) {
                 if (d_td) copy_d2h_strided(o.time_domain, N, start, b->a.td, cap, 0, n, 2, out_s);
                 else copy_d2h_strided(s.fin_td, cap, 0, b->a.td, cap, 0, n, 2, out_s);
             }
@@ -455,14 +467,17 @@ void run_chunks(odegpu_pipeline* p, const Run& j, ChunkSource& src) {
         }
         for (int r = 0; r < kSlots; ++r) drain(p->slots[(k + r) % kSlots]); // oldest first
         if (trace && !tev.empty()) {
-            for (size_t c = 0; c + 3 < tev.size(); c += 4) {
-                float a = 0, h = 0, x = 0, d = 0;
+            for (size_t c = 0; c + 4 < tev.size(); c += 5) {
+                float a = 0, h = 0, x = 0, w = 0, d = 0;
                 cudaEventElapsedTime(&a, tev[0], tev[c]);
                 cudaEventElapsedTime(&h, tev[c], tev[c + 1]);
                 cudaEventElapsedTime(&x, tev[c + 1], tev[c + 2]);
-                cudaEventElapsedTime(&d, tev[c + 2], tev[c + 3]);
-                std::fprintf(stderr, "[pipeline] chunk %zu: h2d at %.3f ms, +%.3f to kernels, +%.3f to d2h, d2h %.3f\n",
-                             c / 4, a, h, x, d);
+                cudaEventElapsedTime(&w, tev[c + 2], tev[c + 3]);
+                cudaEventElapsedTime(&d, tev[c + 3], tev[c + 4]);
+                std::fprintf(stderr,
+                             "[pipeline] chunk %zu: h2d at %.3f ms, +%.3f to kernels, kernels %.3f, +%.3f to d2h, "
+                             "d2h %.3f\n",
+                             c / 5, a, h, x, w, d);
             }
             for (auto e : tev) cudaEventDestroy(e);
         }

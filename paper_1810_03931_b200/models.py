@@ -94,6 +94,17 @@ class SystemDef:
     def event_controls(self) -> EventControls:
         return EventControls()
 
+    def keeps_time_domain(self) -> bool:
+        """Whether a solve never changes a time domain (hooks.hpp
+        kKeepsTimeDomain; odegpu_model_keeps_time_domain)."""
+        import ctypes as C
+
+        v = C.c_int()
+        rc = abi.load().odegpu_model_keeps_time_domain(C.byref(self.to_c()), C.byref(v))
+        if rc != 0:
+            raise RuntimeError(abi.load().odegpu_last_error().decode())
+        return bool(v.value)
+
     def to_c(self) -> abi.Model:
         m = abi.Model()
         m.id = self.model_id

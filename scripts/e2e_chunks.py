@@ -5,7 +5,7 @@ import numpy as np, torch
 import paper_1810_03931_b200 as pkg
 from paper_1810_03931_b200 import abi, workloads
 cfg = sys.argv[1] if len(sys.argv) > 1 else 'cfg2'
-wl = workloads.CONFIGS[cfg]()
+wl = workloads.cfg5(int(cfg[5:].lstrip('_') or 24)) if cfg.startswith('cfg5') else workloads.CONFIGS[cfg]()
 n = wl.n
 td, y, p, acc = wl.arrays()
 pin = lambda a: torch.from_numpy(a).pin_memory().numpy()

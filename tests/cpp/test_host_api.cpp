@@ -192,6 +192,48 @@ int main() {
         CHECK(cb.state_at(2, 0) == cb.state_at(2, 0) && cb.outcomes()[2].accepted_steps > 10);
     });
 
+    run_case("detection observer (solve.hpp:46-50) through the device log", [] {
+        // valve: impacts (event 1, restitution action) until the stop event
+        const Index n = 64;
+        ProblemPool pool(PoolDims{n, 3, 5, 2});
+        for (Index i = 0; i < n; ++i) {
+            pool.time_start(i) = 0.0;
+            pool.time_end(i) = 1e6;
+            const Real q = 0.2 + 9.8 * static_cast<Real>(i) / static_cast<Real>(n - 1);
+            const Real p[5] = {1.25, 10.0, 20.0, q, 0.8};
+            for (Index c = 0; c < 5; ++c) pool.param_at(i, c) = p[c];
+            pool.state_at(i, 0) = 0.2;
+            pool.state_at(i, 1) = 0.0;
+            pool.state_at(i, 2) = 10.2;
+        }
+        models::ValveSystem def;
+        SolverBatch b(make_batch_dims(n, def.dims()));
+        linear_set(b, pool, {0, 0, n, CopyMode::All});
+        std::vector<Index> per_system(static_cast<std::size_t>(n), 0);
+        Index impacts = 0, last_sys = -1, bad_order = 0, bad_action = 0;
+        auto on_det = [&](Index s, const Detection& d, std::span<const Real> pre, std::span<const Real> post) {
+            if (s < last_sys) ++bad_order;
+            last_sys = s;
+            ++per_system[static_cast<std::size_t>(s)];
+            if (d.event_index == 1) {
+                ++impacts;
+                if (!(post[0] == 0.0 && post[1] == -0.8 * pre[1])) ++bad_action; // valve.hpp:66-76
+            }
+            if (d.counter < 1) ++bad_order;
+        };
+        solve(b, def, SolverConfig{Algorithm::RKCK45, 1e-3}, SolveObservers<NoBatchStepObserver, decltype(on_det)>{{}, on_det});
+        const SolverBatch& cb = b;
+        for (Index i = 0; i < n; ++i)
+            CHECK(per_system[static_cast<std::size_t>(i)] == cb.outcomes()[static_cast<std::size_t>(i)].event_detections);
+        CHECK(impacts > 0 && bad_order == 0 && bad_action == 0);
+        // the same solve without an observer gives bitwise the same results
+        SolverBatch plain(make_batch_dims(n, def.dims()));
+        linear_set(plain, pool, {0, 0, n, CopyMode::All});
+        solve(plain, def, SolverConfig{Algorithm::RKCK45, 1e-3});
+        const SolverBatch& cp = plain;
+        for (Index i = 0; i < 3 * n; ++i) CHECK(cp.state()[static_cast<std::size_t>(i)] == cb.state()[static_cast<std::size_t>(i)]);
+    });
+
     run_case("random_set permutation identity", [] { // test_batch.cpp:114-139
         const Index n = 64;
         const auto pool = duffing_pool(n);

@@ -60,12 +60,18 @@ def test_ptxas_reports_no_spills():
     # slot across the RHS's rare slow-division / slow-pow branches (DESIGN.md
     # §3.1). Every certified instantiation, the one the BASELINE workloads
     # run, is spill-free.
+    # Second: the detection-log instantiations (template flag LOG = true,
+    # mangled `Lb1E`), launched only while a batch records detections for an
+    # on_detection observer, may park a few bytes of the commit path.
     def allowed(f, st, ld):
         if st == "0" and ld == "0":
             return True
-        return "rhs_outline" in f and "4TrigE" in f and int(st) <= 8 and int(ld) <= 8
+        if "rhs_outline" in f and "4TrigE" in f and int(st) <= 8 and int(ld) <= 8:
+            return True
+        return "guarded_solve_kernel" in f and "Lb1E" in f and int(st) <= 64 and int(ld) <= 64
     assert all(allowed(*x) for x in ours), [f for f, st, ld in ours if not allowed(f, st, ld)]
     assert all(st == "0" and ld == "0" for f, st, ld in ours if "CertifiedTrig" in f)
+    assert all(st == "0" and ld == "0" for f, st, ld in ours if "guarded_solve_kernel" in f and "Lb0E" in f)
 
 
 def test_struct_layouts():
@@ -177,3 +183,14 @@ def test_c_header_is_plain_c11(tmp_path):
     r = subprocess.run(["gcc", "-std=c11", "-Wall", "-Wextra", "-pedantic", "-Werror", f"-I{root / 'include'}",
                         "-c", str(src), "-o", str(tmp_path / "hc.o")], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_models_that_keep_time_domains():
+    """hooks.hpp kKeepsTimeDomain through the C ABI (no GPU needed): the
+    pipeline skips copying time domains back only for these."""
+    from paper_1810_03931_b200 import workloads
+
+    keeps = {name: workloads.CONFIGS[name]().model.keeps_time_domain() for name in ("cfg1", "cfg2", "cfg3", "cfg4")}
+    # Duffing harness / event models and the valve: initialize writes state
+    # and accessories only; BubbleCollapseSystem's finalize moves t0
+    assert keeps == {"cfg1": True, "cfg2": True, "cfg3": False, "cfg4": True}
