@@ -481,6 +481,7 @@ def main():
         pipe.run(pin_pool, cfg, 1, out_arrays=outs)
         e2e_s += time.perf_counter() - t0
         e2e_steps += int(outc["accepted_steps"].sum() + outc["rejected_steps"].sum())
+    e2e_mode = pipe.last_mode()
     pipe.close()
     (e2e_s,) = allreduce([e2e_s], torch.distributed.ReduceOp.MAX if world > 1 else None)
     (e2e_steps,) = allreduce([e2e_steps], torch.distributed.ReduceOp.SUM if world > 1 else None)
@@ -563,8 +564,14 @@ def main():
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d) * world,
                 "d2h_bytes_per_step": int(d2h) * world, "steps": args.e2e_steps,
-                "path": f"odegpu_pipeline_run over the pinned host pool: {n_chunks} chunks per rank, H2D / "
-                        "kernels / D2H of td, state, accessories and outcome records on separate streams, "
+                "mode": "streaming" if e2e_mode == pkg.api.PIPELINE_STREAMING else "chunked",
+                "path": ("odegpu_pipeline_run over the pinned host pool, STREAMING mode: the pool lands chunk by "
+                         "chunk (copy-in stream, device counter bumped per chunk) while ONE persistent solve kernel "
+                         "runs over it; each chunk's end points and outcome records go back (copy-out stream) as "
+                         "soon as its systems are counted done, "
+                         if e2e_mode == pkg.api.PIPELINE_STREAMING else
+                         f"odegpu_pipeline_run over the pinned host pool: {n_chunks} chunks per rank, H2D / "
+                         "kernels / D2H of td, state, accessories and outcome records on separate streams, ")
                         + ("one in-place iteration per step (end points written back into the pool), "
                            if ip else "") + "wall clock, max over ranks"},
         "cpu_baseline": cpu,

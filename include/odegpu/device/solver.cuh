@@ -52,6 +52,29 @@ struct Controls {
     Index max_steps_in_zone;
 };
 
+/// The streaming gate (odegpu_pipeline STREAMING, csrc/pipeline.cu): the
+/// pool arrives in granules of 2^shift systems while the kernel runs. A lane
+/// takes up system s only once *ready > s >> shift (the copy-in stream
+/// bumps it after each granule group's H2D) and counts s when it is
+/// finished, which releases its group's D2H on the copy-out stream. bad: [0] lowest index with t1 < t0 (~0: none),
+/// [1] systems deferred to the general-trig pass, [2] nonzero: aborted by
+/// the host or timed out. A finished system is counted into
+/// done[group_of[granule]]: one counter (and one stream wait) per copy-out
+/// group. deferred, when non-null (the certified first
+/// pass): systems whose trig arguments exceed the certified range, appended
+/// instead of integrated. packed: every finished system's outcome record in
+/// the reference's 56-byte AoS layout (odegpu_outcome = SystemOutcome,
+/// driver.hpp:34-42), so the D2H ships records without a packing pass.
+struct StreamGate {
+    const unsigned* ready = nullptr;
+    unsigned* done = nullptr;             // per copy-out group (group_of[granule])
+    const unsigned short* group_of = nullptr;
+    unsigned long long* bad = nullptr;
+    unsigned* deferred = nullptr;
+    unsigned char* packed = nullptr;
+    unsigned shift = 0;
+};
+
 /// Device SoA arrays of one batch (stride n): batch.hpp:61-66, outcomes
 /// split per field so every store is coalesced.
 struct BatchArrays {
@@ -103,7 +126,119 @@ struct BatchArrays {
     Real* log_value = nullptr;
     Real* log_y_pre = nullptr;               // [dim][capacity]: state before event_action
     Real* log_y_post = nullptr;              // [dim][capacity]: state after it
+    // When non-null: every finished system's outcome record in the
+    // reference's 56-byte AoS layout (odegpu_outcome = SystemOutcome,
+    // driver.hpp:34-42), written next to the SoA fields at finish, so a
+    // pipeline ships records to the host without a packing pass.
+    unsigned char* packed = nullptr;
+    // Streaming pool (odegpu_pipeline, streaming mode, csrc/pipeline.cu;
+    // the STREAM instantiation only): the pool's granules land while the
+    // kernel runs — StreamGate.
+    StreamGate gate{};
 };
+
+/// kStreamAbort in *gate.ready: the host abandoned the run. A lane that
+/// waits longer than kStreamTimeoutNs for a granule gives up (bad[2]);
+/// either way every system is still counted done, so no copy-out wait is
+/// left hanging.
+constexpr unsigned kStreamAbort = 0x80000000u;
+constexpr unsigned long long kStreamTimeoutNs = 20ull * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+/// Counts a finished (or skipped) system into its granule with release
+/// semantics (MEMBAR.ALL.GPU + REDG; __threadfence would be MEMBAR.SC plus
+/// an L1 invalidation): the system's stores are visible before the count
+/// the copy-out stream waits on.
+__device__ __forceinline__ void stream_release(const StreamGate& g, unsigned sys) {
+    unsigned* const d = g.done + __ldg(g.group_of + (sys >> g.shift));
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(d) : "memory");
+}
+
+/// Per-block shared state of the STREAM instantiation: [0, BLOCK) each
+/// lane's finished system whose count is still pending (+1; 0 = none),
+/// [BLOCK] the highest granule count any lane of the block has seen land.
+template <bool STREAM, int BLOCK>
+__device__ __forceinline__ unsigned* stream_shared() {
+    if constexpr (STREAM) {
+        __shared__ unsigned s[BLOCK + 1];
+        return s;
+    } else {
+        return nullptr;
+    }
+}
+
+/// Waits until the granule holding system `sys` has landed; false when the
+/// run was aborted or the wait timed out (the caller counts the system done
+/// and skips it).
+///
+/// The common case costs no global load: the block remembers the highest
+/// granule count it has seen (`landed`, shared memory). Otherwise one
+/// relaxed load — an acquire would invalidate the SM's whole L1 (CCTL.IVALL
+/// in the SASS). That is safe because no L1 can hold a stale line of a
+/// granule: granules are 2^k >= 32 systems, so every 128-byte line of every
+/// SoA array lies in one granule, and no lane loads a line of a granule
+/// before it has seen that granule land (the loads are control-dependent on
+/// the flag). A lane that had to wait takes one acquire load at the end.
+__device__ __forceinline__ bool stream_wait(const StreamGate& g, unsigned* landed, unsigned sys) {
+    const unsigned need = (sys >> g.shift) + 1u;
+    if (need <= *reinterpret_cast<volatile unsigned*>(landed)) return true;
+    unsigned v = ld_relaxed_gpu(g.ready);
+    unsigned long long t0 = 0;
+    bool waited = false;
+    for (;;) {
+        if (v & kStreamAbort) return false;
+        if (v >= need) break;
+        waited = true;
+        if (*reinterpret_cast<volatile unsigned long long*>(g.bad + 2)) return false;
+        const unsigned long long now = global_ns();
+        if (t0 == 0) {
+            t0 = now;
+        } else if (now - t0 > kStreamTimeoutNs) {
+            atomicOr(g.bad + 2, 1ull);
+            return false;
+        }
+        __nanosleep(400);
+        v = ld_relaxed_gpu(g.ready);
+    }
+    if (waited) v = ld_acquire_gpu(g.ready) & ~kStreamAbort;
+    atomicMax(landed, v);
+    return true;
+}
+
+/// A streaming run's end of one system: its AoS outcome record (when the
+/// run ships outcomes). Its count into the granule follows at the lane's
+/// next fetch (the release fence then finds these stores long performed
+/// instead of stalling the warp on them).
+static __device__ __forceinline__ void stream_finish(const StreamGate& g, unsigned sys, Real final_t, unsigned reason,
+                                                     Index acc, Index rej, Index det, Index secf, Real smallest) {
+    if (g.packed) {
+        unsigned long long* r = reinterpret_cast<unsigned long long*>(g.packed + static_cast<std::size_t>(sys) * 56);
+        r[0] = static_cast<unsigned long long>(__double_as_longlong(final_t));
+        r[1] = reason; // the reason byte and 7 zero pad bytes (little-endian)
+        r[2] = static_cast<unsigned long long>(acc);
+        r[3] = static_cast<unsigned long long>(rej);
+        r[4] = static_cast<unsigned long long>(det);
+        r[5] = static_cast<unsigned long long>(secf);
+        r[6] = static_cast<unsigned long long>(__double_as_longlong(smallest));
+    }
+}
 
 /// Slots of the scan tally (shared with the tally kernel, csrc/kernels.cu).
 enum : int {
@@ -742,7 +877,15 @@ constexpr std::size_t solve_smem_bytes() {
 /// the next step's clipping — so a lane is ready for its next evaluation
 /// without another trip through the state machine. Only detections, stops
 /// and system ends go back through PREPARE.
-template <class H, Algorithm ALG, int BLOCK, class Pol = EffectivePolicy<H>, bool LOG = false>
+///
+/// Bound: in the certified instantiation, the general model whose
+/// trig_argument_bound a streaming run checks per system as it takes it up
+/// (StreamGate::deferred); void otherwise.
+///
+/// STREAM: the streaming-pool instantiation (BatchArrays::gate); the
+/// others carry none of its code.
+template <class H, Algorithm ALG, int BLOCK, class Pol = EffectivePolicy<H>, bool LOG = false, class Bound = void,
+          bool STREAM = false>
 __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, const Controls& c) {
     constexpr int N = H::kSystemDim;
     constexpr int NP = H::kParamCount, NA = H::kAccessoryCount, E = H::kEventCount;
@@ -770,6 +913,35 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
     // stage derivatives of the rolled stage loop (rk_step)
     Real* const kbuf = sh.k + (Pol::kRolledStages ? threadIdx.x : 0);
     const Index n = b.n;
+    // STREAM: pending counts + the block's landed-granule watermark
+    [[maybe_unused]] unsigned* const s_stream = stream_shared<STREAM, BLOCK>();
+    // STREAM: a system's own checks as it is taken up (true: not integrated
+    // — t1 < t0, solve.hpp:159-161, counted done and reported in bad[0]; or,
+    // in the certified instantiation, trig arguments beyond the certified
+    // range: deferred to the general pass). Run on the values the fetch
+    // loads anyway (late) where that is free; before the loads (early) for
+    // models whose parameters live in shared memory, whose register budget
+    // the late form overruns (Keller-Miksis: 16 B of spills).
+    constexpr bool kLateStreamChecks = !Pol::kParamsInShared;
+    [[maybe_unused]] const auto stream_checks = [&](Real t0, Real t1, const Real* p, Index stride, unsigned sys_) {
+        if (t1 < t0) {
+            atomicMin(b.gate.bad, static_cast<unsigned long long>(sys_));
+            stream_release(b.gate, sys_);
+            return true;
+        }
+        if constexpr (!std::is_void_v<Bound>) {
+            if (b.gate.deferred && !(Bound::trig_argument_bound(t0, t1, p, stride) < kTrigCertifiedLimit)) {
+                b.gate.deferred[atomicAdd(b.gate.bad + 1, 1ull)] = sys_;
+                return true;
+            }
+        }
+        return false;
+    };
+    if constexpr (STREAM) {
+        s_stream[threadIdx.x] = 0;
+        if (threadIdx.x == 0) s_stream[BLOCK] = 0;
+        __syncthreads();
+    }
     Real preg[Pol::kParamRegs];
     Real* const prow = Pol::kParamsInShared ? sp + threadIdx.x * Pol::kParamStride : preg;
 
@@ -946,12 +1118,30 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 Index sys;
                 if (phase == kFetch) {
                     const Index j = fetch_system(b.work);
+                    if constexpr (STREAM) { // the count of the system this lane finished last
+                        const unsigned pend = s_stream[threadIdx.x];
+                        if (pend) {
+                            s_stream[threadIdx.x] = 0;
+                            stream_release(b.gate, pend - 1);
+                        }
+                    }
                     if (j >= b.count) {
                         phase = kDone;
                         break;
                     }
                     sys = b.order ? static_cast<Index>(__ldg(b.order + j)) : j;
-                    if (b.reason[sys] == static_cast<std::uint8_t>(StopReason::NonFiniteAbort)) continue; // solve.hpp:98
+                    if constexpr (STREAM) { // streaming pool: the system's granule must have landed
+                        if (!stream_wait(b.gate, s_stream + BLOCK, static_cast<unsigned>(sys))) {
+                            stream_release(b.gate, static_cast<unsigned>(sys));
+                            continue;
+                        }
+                        if constexpr (!kLateStreamChecks) {
+                            const Real t0 = b.td[sys], t1 = b.td[sys + n];
+                            if (stream_checks(t0, t1, b.params + sys, n, static_cast<unsigned>(sys))) continue;
+                        }
+                    }
+                    // solve.hpp:98 (never in a streaming run: it resets every outcome first)
+                    if (b.reason[sys] == static_cast<std::uint8_t>(StopReason::NonFiniteAbort)) continue;
                     ODEGPU_C(it_left) = static_cast<unsigned short>(b.iterations);
                 } else {
                     sys = static_cast<Index>(ODEGPU_C(sys));
@@ -966,6 +1156,8 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 Real acc[A];
 #pragma unroll
                 for (int i = 0; i < NA; ++i) acc[i] = b.acc[sys + i * n];
+                if constexpr (STREAM && kLateStreamChecks)
+                    if (phase == kFetch && stream_checks(td[0], td[1], prow, 1, static_cast<unsigned>(sys))) continue;
                 ODEGPU_B(n_acc) = ODEGPU_B(n_rej) = 0u;
                 ODEGPU_C(acc_hi) = ODEGPU_C(rej_hi) = 0u;
                 ODEGPU_C(n_det) = ODEGPU_C(n_secf) = 0ull;
@@ -1121,6 +1313,13 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                 phase = (left > 0 && ODEGPU_C(reason) != static_cast<std::uint8_t>(StopReason::NonFiniteAbort))
                             ? kRefetch
                             : kFetch;
+                if constexpr (STREAM) // the system's last solve of this launch
+                    if (phase == kFetch) {
+                        stream_finish(b.gate, static_cast<unsigned>(sys), t, ODEGPU_C(reason), acc64, rej64,
+                                      static_cast<Index>(ODEGPU_C(n_det)), static_cast<Index>(ODEGPU_C(n_secf)),
+                                      ODEGPU_B(smallest));
+                        s_stream[threadIdx.x] = static_cast<unsigned>(sys) + 1u; // counted at the next fetch
+                    }
                 continue;
             }
             if (phase == kSecant) {
@@ -1377,19 +1576,23 @@ __global__ void trig_certificate_kernel(BatchArrays b, unsigned long long* flags
 /// log_*, the reference's on_detection observer), launched only while a
 /// batch has a detection log — like the reference's `observing` branch
 /// (driver.hpp:186-206) it costs nothing when nobody observes.
-template <class H, Algorithm ALG, int BLOCK, int MIN_BLOCKS, bool LOG = false>
+///
+/// STREAM: the streaming-pool instantiation (odegpu_pipeline STREAMING):
+/// lanes wait on the chunk gate, check t1 < t0 and (certified path) the
+/// trig bound per system, and write packed records and chunk counts.
+template <class H, Algorithm ALG, int BLOCK, int MIN_BLOCKS, bool LOG = false, bool STREAM = false>
 __global__ void __launch_bounds__(BLOCK, MIN_BLOCKS)
     guarded_solve_kernel(H model, BatchArrays b, Controls c, const unsigned long long* flags) {
     if (flags[0] != ~0ull) return;
     dmath::init_shared_tables();
     if constexpr (TrigCertifiable<H>) {
         if (flags[1] == 0) {
-            solve_lanes<typename H::certified_hooks, ALG, BLOCK, EffectivePolicy<H>, LOG>(
+            solve_lanes<typename H::certified_hooks, ALG, BLOCK, EffectivePolicy<H>, LOG, H, STREAM>(
                 typename H::certified_hooks{}, b, c);
             return;
         }
     }
-    solve_lanes<H, ALG, BLOCK, EffectivePolicy<H>, LOG>(model, b, c);
+    solve_lanes<H, ALG, BLOCK, EffectivePolicy<H>, LOG, void, STREAM>(model, b, c);
 }
 
 /// Kernel controls from the C-ABI structs (materialised once per solve,

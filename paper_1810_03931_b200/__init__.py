@@ -13,6 +13,9 @@ from .api import (  # noqa: F401
     LinearCopySpec,
     OdegpuError,
     OutOfRange,
+    Pipeline,
+    Unsupported,
+    pinned,
     PoolDims,
     ProblemPool,
     RandomCopySpec,

@@ -335,6 +335,8 @@ def _bind(lib):
              C.c_uint32, CHUNK_SINK, vp],
         ),
         "odegpu_pipeline_destroy": (None, [vp]),
+        "odegpu_pipeline_set_mode": (C.c_int, [vp, C.c_int32]),
+        "odegpu_pipeline_last_mode": (C.c_int, [vp, P(C.c_int32)]),
         "odegpu_pipeline_run_tallied": (
             C.c_int,
             [vp, P(PoolView), P(PoolOut), P(SolverConfig), P(OdeControls), P(EventControls), Index, Index,
@@ -353,7 +355,12 @@ def _bind(lib):
         "odegpu_host_register": (C.c_int, [vp, C.c_size_t]),
         "odegpu_host_unregister": (C.c_int, [vp]),
     }
+    # an older tuning variant (ODEGPU_LIB=lib/variants/*.so, A/B runs) may
+    # lack newer entry points; the in-tree library must export them all
+    variant = "variants" in Path(os.environ.get("ODEGPU_LIB", "")).parts
     for name, (res, args) in sig.items():
+        if variant and not hasattr(lib, name):
+            continue
         f = getattr(lib, name)
         f.restype = res
         f.argtypes = args

@@ -13,6 +13,8 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass
 
+import weakref
+
 import numpy as np
 
 from . import abi
@@ -180,6 +182,13 @@ class ProblemPool:
             abi.dptr(self._acc if self._acc.size else None))
         v._keep = self
         return v
+
+    def pin(self) -> "ProblemPool":
+        """Moves the pool's arrays into page-locked host memory (pinned()),
+        so pipeline copies are asynchronous and the streaming mode applies."""
+        self._td, self._state, self._params, self._acc = (pinned(a) for a in (self._td, self._state, self._params,
+                                                                                  self._acc))
+        return self
 
     @staticmethod
     def from_arrays(td, y, p, acc) -> "ProblemPool":
@@ -569,6 +578,26 @@ def slice_range(total: int, parts: int, index: int) -> tuple[int, int]:
 RECORD_TD, RECORD_STATE, RECORD_ACC, RECORD_OUTCOMES = 1, 2, 8, 16
 
 
+_PAGE = 4096
+
+
+def pinned(a: np.ndarray) -> np.ndarray:
+    """A page-locked copy of `a` (odegpu_host_register over page-aligned
+    numpy storage of its own, unregistered when the copy is collected)."""
+    a = np.asarray(a)
+    nbytes = max(a.nbytes, 1)
+    span = -(-nbytes // _PAGE) * _PAGE
+    raw = np.empty(span + _PAGE, dtype=np.uint8)
+    off = (-raw.ctypes.data) % _PAGE
+    buf = raw[off:off + span]
+    lib = abi.load()
+    check(lib.odegpu_host_register(C.c_void_p(buf.ctypes.data), span))
+    weakref.finalize(raw, lib.odegpu_host_unregister, C.c_void_p(buf.ctypes.data))
+    out = buf[:a.nbytes].view(a.dtype).reshape(a.shape)
+    out[...] = a
+    return out
+
+
 def _pool_out(defn, n, arrays=None):
     d = defn.dims()
     if arrays is None:
@@ -604,17 +633,32 @@ def _chunk_sink(defn, record_mask, on_chunk, err):
     return abi.CHUNK_SINK(_sink) if on_chunk else abi.CHUNK_SINK()
 
 
-class Pipeline:
-    """Persistent chunked pipeline (odegpu_pipeline_*): two device batches of
-    `batch_capacity` systems, two streams and pinned staging, reused by every
-    run() — chunk k+1's H2D and chunk k-1's D2H overlap chunk k's kernels."""
+PIPELINE_AUTO, PIPELINE_CHUNKED, PIPELINE_STREAMING = 0, 1, 2  # enum odegpu_pipeline_mode
 
-    def __init__(self, defn: SystemDef, batch_capacity: int, device: int = 0):
+
+class Pipeline:
+    """Persistent pool pipeline (odegpu_pipeline_*), reused by every run().
+    CHUNKED: device batches of `batch_capacity` systems, chunk k+1's H2D and
+    chunk k-1's D2H overlap chunk k's kernels. STREAMING: the pool becomes
+    resident while one persistent solve kernel runs over it, gated chunk by
+    chunk on the copies. AUTO (the default) runs the chunked slots; STREAMING is opt-in."""
+
+    def __init__(self, defn: SystemDef, batch_capacity: int, device: int = 0, mode: int = PIPELINE_AUTO):
         self._lib = abi.load()
         self.defn = defn
         h = C.c_void_p()
         check(self._lib.odegpu_pipeline_create(C.byref(defn.to_c()), batch_capacity, device, C.byref(h)))
         self._h = h
+        if mode != PIPELINE_AUTO:
+            self.set_mode(mode)
+
+    def set_mode(self, mode: int):
+        check(self._lib.odegpu_pipeline_set_mode(self._h, mode))
+
+    def last_mode(self) -> int:
+        m = C.c_int32()
+        check(self._lib.odegpu_pipeline_last_mode(self._h, C.byref(m)))
+        return m.value
 
     def close(self):
         if getattr(self, "_h", None):

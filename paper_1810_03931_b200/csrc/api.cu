@@ -77,6 +77,15 @@ bool keeps_time_domain(const odegpu_model& m) {
     throw_unsupported("unknown model id " + std::to_string(m.id));
 }
 
+bool fusable_iterations(const odegpu_model& m) {
+    odegpu_system_dims d{};
+    bool keeps = false, fusable = false;
+    if (family_dims_duffing(m, &d, &keeps, &fusable) || family_dims_keller_miksis(m, &d, &keeps, &fusable) ||
+        family_dims_valve(m, &d, &keeps, &fusable) || family_dims_fakes(m, &d, &keeps, &fusable))
+        return fusable;
+    throw_unsupported("unknown model id " + std::to_string(m.id));
+}
+
 void launch_model(odegpu_batch* b, const odegpu_model& m, int algorithm, const dev::Controls& c) {
     if (family_launch_duffing(b, m, algorithm, c) || family_launch_keller_miksis(b, m, algorithm, c) ||
         family_launch_valve(b, m, algorithm, c) || family_launch_fakes(b, m, algorithm, c))

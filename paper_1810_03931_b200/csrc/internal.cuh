@@ -103,6 +103,11 @@ struct odegpu_batch {
     odegpu::Index fused_done = 1;
     unsigned long long* trial_steps = nullptr; // device: trial steps integrated since the last reset
     void* log_block = nullptr; // detection log (odegpu_batch_set_detection_log), BatchArrays::log_*
+    // streaming pool run (pipeline.cu): 1 = the pass over the arriving
+    // chunks, 2 = the general-trig pass over the systems it deferred; the
+    // launch then skips the certificate pre-pass and fetches in stream_order
+    int stream_mode = 0;
+    const unsigned* stream_order = nullptr;
 };
 
 namespace odegpu::detail {
@@ -130,10 +135,10 @@ void launch_tally(odegpu_batch* b, unsigned long long* tally, bool chunk_end); /
 double run_dfma_peak(int blocks, int threads, int iters, double* seconds);
 
 // ---- model translation units: widths and kernel dispatch per model family
-bool family_dims_duffing(const odegpu_model& m, odegpu_system_dims* d, bool* keeps = nullptr);
-bool family_dims_keller_miksis(const odegpu_model& m, odegpu_system_dims* d, bool* keeps = nullptr);
-bool family_dims_valve(const odegpu_model& m, odegpu_system_dims* d, bool* keeps = nullptr);
-bool family_dims_fakes(const odegpu_model& m, odegpu_system_dims* d, bool* keeps = nullptr);
+bool family_dims_duffing(const odegpu_model& m, odegpu_system_dims* d, bool* keeps = nullptr, bool* fusable = nullptr);
+bool family_dims_keller_miksis(const odegpu_model& m, odegpu_system_dims* d, bool* keeps = nullptr, bool* fusable = nullptr);
+bool family_dims_valve(const odegpu_model& m, odegpu_system_dims* d, bool* keeps = nullptr, bool* fusable = nullptr);
+bool family_dims_fakes(const odegpu_model& m, odegpu_system_dims* d, bool* keeps = nullptr, bool* fusable = nullptr);
 bool family_launch_duffing(odegpu_batch* b, const odegpu_model& m, int alg, const dev::Controls& c);
 bool family_launch_keller_miksis(odegpu_batch* b, const odegpu_model& m, int alg, const dev::Controls& c);
 bool family_launch_valve(odegpu_batch* b, const odegpu_model& m, int alg, const dev::Controls& c);
@@ -143,6 +148,8 @@ bool family_launch_fakes(odegpu_batch* b, const odegpu_model& m, int alg, const 
 odegpu_system_dims dims_of(const odegpu_model& m);
 // whether a solve of the model leaves time domains unchanged (hooks.hpp kKeepsTimeDomain)
 bool keeps_time_domain(const odegpu_model& m);
+// whether solve_iteratively may fuse the model's iterations into one launch (hooks.hpp kFusableIterations)
+bool fusable_iterations(const odegpu_model& m);
 void launch_model(odegpu_batch* b, const odegpu_model& m, int algorithm, const dev::Controls& c);
 dev::Controls prepare_solve(const odegpu_batch_dims& d, const odegpu_model* m, const odegpu_solver_config* cfg,
                             const odegpu_ode_controls* ode, const odegpu_event_controls* ev);

@@ -50,16 +50,21 @@ void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
     // launch bounds leave it one block per SM fewer (more registers for the
     // observer path instead of spills)
     const bool log = H::kEventCount > 0 && b->a.log_count != nullptr;
-    auto kern = guarded_solve_kernel<H, ALG, kBlock, kMin, false>;
+    // streaming pool (pipeline.cu): its own instantiation; the caller has set
+    // both flags and the fetch order, the certificate is checked per system
+    const bool streaming = b->stream_mode != 0;
+    auto kern = guarded_solve_kernel<H, ALG, kBlock, kMin, false, false>;
     if constexpr (H::kEventCount > 0)
-        if (log) kern = guarded_solve_kernel<H, ALG, kBlock, (kMin > 1 ? kMin - 1 : 1), true>;
+        if (log) kern = guarded_solve_kernel<H, ALG, kBlock, (kMin > 1 ? kMin - 1 : 1), true, false>;
+    if (streaming) kern = guarded_solve_kernel<H, ALG, kBlock, kMin, false, true>;
+    const int variant = streaming ? 2 : log ? 1 : 0;
     constexpr std::size_t smem = dev::solve_smem_bytes<H, ALG, kBlock>();
     if constexpr (smem > 48 * 1024) // opt-in above the static limit (per device)
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     // resident blocks per SM, per instantiation and device: device threads of
     // odegpu_solve_pool_multi launch concurrently, and devices may differ
-    static std::atomic<int> resident_of[2][kMaxDevices] = {};
-    auto& cache = resident_of[log ? 1 : 0];
+    static std::atomic<int> resident_of[3][kMaxDevices] = {};
+    auto& cache = resident_of[variant];
     int resident = b->device >= 0 && b->device < kMaxDevices ? cache[b->device].load(std::memory_order_relaxed) : 0;
     if (resident <= 0) {
         int r = 0;
@@ -71,7 +76,7 @@ void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
     const Index persistent = Index(b->num_sms) * resident;
     const Index needed = (n + kBlock - 1) / kBlock;
     const int grid = static_cast<int>(std::max<Index>(1, std::min(needed, persistent)));
-    if constexpr (dev::TrigCertifiable<H>) {
+    if constexpr (dev::TrigCertifiable<H>) if (!streaming) {
         CK(cudaMemsetAsync(b->first_bad + 1, 0, sizeof(unsigned long long), b->stream));
         dev::trig_certificate_kernel<H><<<grid_for(b, b->a.count, 256), 256, 0, b->stream>>>(b->a, b->first_bad);
         CK(cudaGetLastError());
@@ -85,8 +90,9 @@ void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
             return LaunchPolicy<H>::kCostOrder && ALG == Algorithm::RKCK45;
         else return false;
     }();
-    const bool cost = b->order_mode == ODEGPU_FETCH_COST || (b->order_mode == ODEGPU_FETCH_AUTO && kPolicyCost);
-    b->a.order = (cost && b->order_count == n) ? b->order : nullptr;
+    const bool cost = !streaming && (b->order_mode == ODEGPU_FETCH_COST ||
+                                     (b->order_mode == ODEGPU_FETCH_AUTO && kPolicyCost));
+    b->a.order = streaming ? b->stream_order : (cost && b->order_count == n) ? b->order : nullptr;
     b->a.cost = (cost && b->build_order) ? b->cost : nullptr; // null until the first order build allocates it
     // fused iterations: the systems of this launch are solved `fused` times
     // in a row (hooks.hpp kFusableIterations; one solve otherwise)
@@ -121,9 +127,10 @@ void launch_alg(odegpu_batch* b, const H& hooks, int algorithm, const dev::Contr
 }
 
 template <class H>
-void set_dims(odegpu_system_dims* d, bool* keeps_time_domain = nullptr) {
+void set_dims(odegpu_system_dims* d, bool* keeps_time_domain = nullptr, bool* fusable = nullptr) {
     *d = odegpu_system_dims{H::kSystemDim, H::kParamCount, H::kEventCount, H::kAccessoryCount};
     if (keeps_time_domain) *keeps_time_domain = kKeepsTimeDomain<H>;
+    if (fusable) *fusable = kFusableIterations<H>;
 }
 
 } // namespace odegpu::detail

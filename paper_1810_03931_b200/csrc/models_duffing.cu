@@ -49,13 +49,13 @@ struct LaunchPolicy<models::DuffingLyapunovHooks> {
     static constexpr bool kCostOrder = true;
 };
 
-bool family_dims_duffing(const odegpu_model& m, odegpu_system_dims* d, bool* keeps) {
+bool family_dims_duffing(const odegpu_model& m, odegpu_system_dims* d, bool* keeps, bool* fusable) {
     switch (m.id) {
-    case ODEGPU_MODEL_DUFFING: set_dims<models::DuffingHooks>(d, keeps); return true;
-    case ODEGPU_MODEL_DUFFING_MAX_ACCESSORY: set_dims<models::DuffingMaxAccessoryHooks>(d, keeps); return true;
-    case ODEGPU_MODEL_DUFFING_MAX_EVENT: set_dims<models::DuffingMaxEventHooks>(d, keeps); return true;
-    case ODEGPU_MODEL_DUFFING_MAXMIN: set_dims<models::DuffingMaxMinHooks>(d, keeps); return true;
-    case ODEGPU_MODEL_DUFFING_LYAPUNOV: set_dims<models::DuffingLyapunovHooks>(d, keeps); return true;
+    case ODEGPU_MODEL_DUFFING: set_dims<models::DuffingHooks>(d, keeps, fusable); return true;
+    case ODEGPU_MODEL_DUFFING_MAX_ACCESSORY: set_dims<models::DuffingMaxAccessoryHooks>(d, keeps, fusable); return true;
+    case ODEGPU_MODEL_DUFFING_MAX_EVENT: set_dims<models::DuffingMaxEventHooks>(d, keeps, fusable); return true;
+    case ODEGPU_MODEL_DUFFING_MAXMIN: set_dims<models::DuffingMaxMinHooks>(d, keeps, fusable); return true;
+    case ODEGPU_MODEL_DUFFING_LYAPUNOV: set_dims<models::DuffingLyapunovHooks>(d, keeps, fusable); return true;
     default: return false;
     }
 }

@@ -22,18 +22,18 @@ struct KernelPolicy<fakes::RampHooks> {
 
 namespace odegpu::detail {
 
-bool family_dims_fakes(const odegpu_model& m, odegpu_system_dims* d, bool* keeps) {
+bool family_dims_fakes(const odegpu_model& m, odegpu_system_dims* d, bool* keeps, bool* fusable) {
     switch (m.id) {
-    case ODEGPU_MODEL_CONSTANT: set_dims<fakes::ConstantHooks>(d, keeps); return true;
-    case ODEGPU_MODEL_CUBIC_TIME: set_dims<fakes::CubicTimeHooks>(d, keeps); return true;
-    case ODEGPU_MODEL_EXPONENTIAL: set_dims<fakes::ExponentialHooks>(d, keeps); return true;
-    case ODEGPU_MODEL_UNIT_SLOPE: set_dims<fakes::UnitSlopeHooks>(d, keeps); return true;
-    case ODEGPU_MODEL_COUNTING: set_dims<fakes::CountingHooks>(d, keeps); return true;
-    case ODEGPU_MODEL_RAMP: set_dims<fakes::RampHooks>(d, keeps); return true;
-    case ODEGPU_MODEL_DECAY: set_dims<fakes::DecayHooks>(d, keeps); return true;
-    case ODEGPU_MODEL_SEAT_CONTACT: set_dims<fakes::SeatContactHooks>(d, keeps); return true;
-    case ODEGPU_MODEL_HARMONIC: set_dims<fakes::HarmonicHooks>(d, keeps); return true;
-    case ODEGPU_MODEL_BLOWUP: set_dims<fakes::BlowUpHooks>(d, keeps); return true;
+    case ODEGPU_MODEL_CONSTANT: set_dims<fakes::ConstantHooks>(d, keeps, fusable); return true;
+    case ODEGPU_MODEL_CUBIC_TIME: set_dims<fakes::CubicTimeHooks>(d, keeps, fusable); return true;
+    case ODEGPU_MODEL_EXPONENTIAL: set_dims<fakes::ExponentialHooks>(d, keeps, fusable); return true;
+    case ODEGPU_MODEL_UNIT_SLOPE: set_dims<fakes::UnitSlopeHooks>(d, keeps, fusable); return true;
+    case ODEGPU_MODEL_COUNTING: set_dims<fakes::CountingHooks>(d, keeps, fusable); return true;
+    case ODEGPU_MODEL_RAMP: set_dims<fakes::RampHooks>(d, keeps, fusable); return true;
+    case ODEGPU_MODEL_DECAY: set_dims<fakes::DecayHooks>(d, keeps, fusable); return true;
+    case ODEGPU_MODEL_SEAT_CONTACT: set_dims<fakes::SeatContactHooks>(d, keeps, fusable); return true;
+    case ODEGPU_MODEL_HARMONIC: set_dims<fakes::HarmonicHooks>(d, keeps, fusable); return true;
+    case ODEGPU_MODEL_BLOWUP: set_dims<fakes::BlowUpHooks>(d, keeps, fusable); return true;
     default: return false;
     }
 }

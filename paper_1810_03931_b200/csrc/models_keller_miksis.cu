@@ -46,10 +46,10 @@ static_assert(5 * (dev::solve_smem_bytes<models::BubbleCollapseHooks, Algorithm:
                   228 * 1024,
               "Keller-Miksis shared-memory layout no longer fits 5 blocks per SM");
 
-bool family_dims_keller_miksis(const odegpu_model& m, odegpu_system_dims* d, bool* keeps) {
+bool family_dims_keller_miksis(const odegpu_model& m, odegpu_system_dims* d, bool* keeps, bool* fusable) {
     switch (m.id) {
-    case ODEGPU_MODEL_KELLER_MIKSIS: set_dims<models::KellerMiksisHooks>(d, keeps); return true;
-    case ODEGPU_MODEL_BUBBLE_COLLAPSE: set_dims<models::BubbleCollapseHooks>(d, keeps); return true;
+    case ODEGPU_MODEL_KELLER_MIKSIS: set_dims<models::KellerMiksisHooks>(d, keeps, fusable); return true;
+    case ODEGPU_MODEL_BUBBLE_COLLAPSE: set_dims<models::BubbleCollapseHooks>(d, keeps, fusable); return true;
     default: return false;
     }
 }

@@ -24,9 +24,9 @@ struct LaunchPolicy<models::ValveHooks> {
     static constexpr bool kCostOrder = true; // step counts spread widely: longest first
 };
 
-bool family_dims_valve(const odegpu_model& m, odegpu_system_dims* d, bool* keeps) {
+bool family_dims_valve(const odegpu_model& m, odegpu_system_dims* d, bool* keeps, bool* fusable) {
     if (m.id != ODEGPU_MODEL_VALVE) return false;
-    set_dims<models::ValveHooks>(d, keeps);
+    set_dims<models::ValveHooks>(d, keeps, fusable);
     return true;
 }
 

@@ -2,6 +2,7 @@
 // src/scan.cpp:88-112 run_chunks) with double-buffered H2D/D2H on two
 // streams, and its multi-GPU form (one host thread and one contiguous slice
 // per device; no inter-GPU traffic: systems are independent).
+#include <cuda.h> // stream memory operation types only (entry points via cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -145,6 +146,38 @@ struct Slot {
     bool busy = false;
 };
 
+/// The streaming mode's device state (odegpu_pipeline_mode STREAMING): one
+/// batch holding the whole pool, the chunk gate and the packed records.
+constexpr cuuint32_t kStreamAbortHost = 0x80000000u; // dev::kStreamAbort
+
+struct StreamState {
+    static constexpr Index kMaxGranules = 256;
+    odegpu_batch* batch = nullptr;
+    Index cap = 0;
+    unsigned* gate = nullptr;               // [0] chunks landed, [1 + c] systems of chunk c finished
+    unsigned long long* bad = nullptr;      // BatchArrays::stream_bad (4 words)
+    unsigned long long* h_bad = nullptr;    // pinned mirror
+    unsigned short* group_of = nullptr;     // [kMaxGranules] granule -> copy-out group (device)
+    unsigned short* h_group_of = nullptr;   // pinned staging
+    unsigned* deferred = nullptr;           // [cap]
+    unsigned char* packed = nullptr;        // [cap] x 56 B
+    cudaEvent_t prologue = nullptr;
+    void release() {
+        if (batch) {
+            cudaStreamSynchronize(batch->stream);
+            odegpu_batch_destroy(batch);
+        }
+        for (void* q : {static_cast<void*>(gate), static_cast<void*>(bad), static_cast<void*>(deferred),
+                        static_cast<void*>(packed)})
+            if (q) cudaFree(q);
+        if (h_bad) cudaFreeHost(h_bad);
+        if (group_of) cudaFree(group_of);
+        if (h_group_of) cudaFreeHost(h_group_of);
+        if (prologue) cudaEventDestroy(prologue);
+        *this = StreamState{};
+    }
+};
+
 struct Run {
     const odegpu_pool_view* pool;
     const odegpu_pool_out* out;
@@ -175,8 +208,12 @@ struct odegpu_pipeline {
     std::vector<odegpu_outcome> packed;
     unsigned long long* d_tally = nullptr; // device scan tally (kTallySlots counters)
     unsigned long long* h_tally = nullptr; // pinned mirror
+    int32_t mode = ODEGPU_PIPELINE_AUTO;      // odegpu_pipeline_set_mode
+    int32_t last_mode = ODEGPU_PIPELINE_AUTO; // what the last run used
+    odegpu::detail::StreamState stream;       // streaming mode, allocated on first use
 
     ~odegpu_pipeline() {
+        stream.release();
         for (auto& s : slots) {
             if (s.batch) {
                 cudaStreamSynchronize(s.batch->stream);
@@ -512,7 +549,359 @@ void run_chunks(odegpu_pipeline* p, const Run& j, ChunkSource& src) {
     }
 }
 
+// ---------------------------------------------------------------- streaming
+
+using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+/// cuStreamWriteValue32 / cuStreamWaitValue32 from the driver the runtime
+/// runs on (no link-time dependency on libcuda); null when unavailable.
+struct StreamMemOps {
+    WriteValueFn write = nullptr;
+    WaitValueFn wait = nullptr;
+};
+
+const StreamMemOps& stream_memops() {
+    static const StreamMemOps ops = [] {
+        StreamMemOps o;
+        void* w = nullptr;
+        void* v = nullptr;
+        cudaDriverEntryPointQueryResult q1{}, q2{};
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+            cudaGetDriverEntryPoint("cuStreamWaitValue32", &v, cudaEnableDefault, &q2) == cudaSuccess &&
+            q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && w && v) {
+            o.write = reinterpret_cast<WriteValueFn>(w);
+            o.wait = reinterpret_cast<WaitValueFn>(v);
+        }
+        cudaGetLastError();
+        return o;
+    }();
+    return ops;
+}
+
+void check_cu(CUresult r, const char* what) {
+    if (r != CUDA_SUCCESS) throw Error(ODEGPU_ERR_CUDA, std::string(what) + ": CUresult " + std::to_string(int(r)));
+}
+
+/// Device bytes per system of the streaming batch and its side arrays.
+Index stream_bytes_per_system(const odegpu_system_dims& sd) {
+    return 8 * (2 + sd.system_dim + sd.param_count + sd.accessory_count) + 49 + 56 + 4 + 16;
+}
+
+/// Why the streaming mode does not apply to this run (nullptr: it does).
+const char* stream_blocker(odegpu_pipeline* p, const Run& j) {
+    if (j.sink || j.tally) return "a chunk sink or scan tally needs per-chunk iterations";
+    if (j.iterations > 1 && !fusable_iterations(p->model)) return "the model's iterations do not fuse";
+    if (j.iterations > 65535) return "more than 65535 fused iterations";
+    const Index N = j.pool->dims.problem_size;
+    if (N >= (Index(1) << 31)) return "pool too large for 32-bit system indices";
+    const odegpu_system_dims& sd = p->sd;
+    if (!is_pinned(j.pool->time_domain) || !is_pinned(j.pool->state) ||
+        (sd.param_count && !is_pinned(j.pool->parameters)) || (sd.accessory_count && !is_pinned(j.pool->accessories)))
+        return "pool arrays are not page-locked";
+    if (j.out) {
+        const odegpu_pool_out& o = *j.out;
+        if ((o.time_domain && !is_pinned(o.time_domain)) || (o.state && !is_pinned(o.state)) ||
+            (o.accessories && sd.accessory_count && !is_pinned(o.accessories)) ||
+            (o.outcomes && !is_pinned(o.outcomes)))
+            return "out arrays are not page-locked";
+    }
+    const StreamMemOps& ops = stream_memops();
+    if (!ops.write || !ops.wait) return "stream memory operations unavailable";
+    if (p->stream.cap < N) {
+        size_t free_b = 0, total_b = 0;
+        DeviceGuard g(p->device);
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        const double have = double(free_b) + (p->stream.batch ? double(p->stream.cap) * double(stream_bytes_per_system(sd)) : 0.0);
+        if (double(N) * double(stream_bytes_per_system(sd)) > 0.6 * have) return "pool does not fit the device";
+    }
+    return nullptr;
+}
+
+/// (Re)allocates the streaming state for N systems.
+void stream_reserve(odegpu_pipeline* p, Index N) {
+    StreamState& st = p->stream;
+    if (st.batch && st.cap >= N) return;
+    st.release();
+    DeviceGuard g(p->device);
+    const auto& sd = p->sd;
+    const odegpu_batch_dims bd{N, sd.system_dim, sd.param_count, sd.event_count, sd.accessory_count};
+    try {
+        st.batch = batch_create(bd, p->device);
+        st.cap = N;
+        CK(cudaMalloc(&st.gate, sizeof(unsigned) * (1 + StreamState::kMaxGranules)));
+        CK(cudaMalloc(&st.bad, 4 * sizeof(unsigned long long)));
+        CK(cudaMallocHost(&st.h_bad, 4 * sizeof(unsigned long long)));
+        CK(cudaMalloc(&st.group_of, sizeof(unsigned short) * StreamState::kMaxGranules));
+        CK(cudaMallocHost(&st.h_group_of, sizeof(unsigned short) * StreamState::kMaxGranules));
+        CK(cudaMalloc(&st.deferred, sizeof(unsigned) * size_t(N)));
+        CK(cudaMalloc(&st.packed, 56 * size_t(N)));
+        CK(cudaEventCreateWithFlags(&st.prologue, cudaEventDisableTiming));
+    } catch (...) {
+        st.release();
+        throw;
+    }
+}
+
+/// log2 of the systems per granule of a streamed pool: N/256 rounded up to
+/// a power of two, at least 4096 (cfg2's 2^20 pool: 16 Ki systems, 1.3 MB
+/// of inputs) and 32 — every 128-byte line of every SoA array lies in one
+/// granule, and a lane finds its granule with a shift. ODEGPU_STREAM_CHUNK
+/// overrides the size (tuning; rounded up to a power of two).
+unsigned stream_granule_shift(Index N) {
+    Index s = std::max<Index>((N + StreamState::kMaxGranules - 1) / StreamState::kMaxGranules, 4096);
+    if (const char* e = std::getenv("ODEGPU_STREAM_CHUNK")) s = std::max<Index>(1, std::atoll(e));
+    unsigned k = 5;
+    while ((Index(1) << k) < s || (N + (Index(1) << k) - 1) >> k > StreamState::kMaxGranules) ++k;
+    return k;
+}
+
+/// Granule groups moved by one copy each: small first (H2D: the kernel's
+/// lanes start on the first granule within tens of microseconds), doubling
+/// up to kMaxGroup granules (copies of several MB run at full PCIe rate),
+/// and for the copy-out the mirror image — small last, so the D2H left
+/// after the kernel's final systems is one granule or two.
+std::vector<std::pair<Index, Index>> granule_groups(Index ng, bool small_last) {
+    // ODEGPU_STREAM_GROUP_IN / _OUT override the cap (tuning)
+    const char* env = std::getenv(small_last ? "ODEGPU_STREAM_GROUP_OUT" : "ODEGPU_STREAM_GROUP_IN");
+    const Index kMaxGroup = env ? std::max<Index>(1, std::atoll(env)) : 16;
+    std::vector<Index> sizes;
+    for (Index g = 0, sz = 1; g < ng; g += sizes.back(), sz = std::min<Index>(2 * sz, kMaxGroup))
+        sizes.push_back(std::min(sz, ng - g));
+    if (small_last) std::reverse(sizes.begin(), sizes.end());
+    std::vector<std::pair<Index, Index>> out;
+    Index g = 0;
+    for (Index z : sizes) {
+        out.emplace_back(g, g + z);
+        g += z;
+    }
+    return out;
+}
+
+/// The streaming mode (odegpu_pipeline_mode STREAMING): the whole pool
+/// becomes resident in one batch while one persistent solve kernel runs.
+/// The pool is cut into granules of 2^shift systems:
+///   compute stream: reset gate / flags / outcomes -> [prologue event] ->
+///                   solve kernel (a lane takes up a system once its
+///                   granule has landed, counts it done when finished)
+///   copy-in:        [prologue] -> H2D of a granule group -> gate[0] = its
+///                   end (cuStreamWriteValue32), group after group
+///   copy-out:       [prologue] -> for a granule group: wait gate[1 + g] >=
+///                   granule size for each g (cuStreamWaitValue32) -> D2H
+/// Systems the certified kernel defers (trig arguments beyond the certified
+/// range) run afterwards in a second launch of the general instantiation
+/// over the deferred list; their granules' D2H wait for it.
+void run_streaming(odegpu_pipeline* p, const Run& j) {
+    const odegpu_pool_dims& pd = j.pool->dims;
+    const odegpu_system_dims& sd = p->sd;
+    const Index N = pd.problem_size;
+    const StreamMemOps& ops = stream_memops();
+    DeviceGuard g(p->device);
+    stream_reserve(p, N);
+    StreamState& st = p->stream;
+    odegpu_batch* b = st.batch;
+    const Index cap = st.cap;
+    const odegpu_batch_dims bd{cap, sd.system_dim, sd.param_count, sd.event_count, sd.accessory_count};
+    const dev::Controls c = prepare_solve(bd, &p->model, j.cfg, j.ode, j.ev);
+    const unsigned shift = stream_granule_shift(N);
+    const Index G = Index(1) << shift, NG = (N + G - 1) / G;
+    const auto in_groups = granule_groups(NG, false), out_groups = granule_groups(NG, true);
+    const odegpu_pool_out none{};
+    const odegpu_pool_out& o = j.out ? *j.out : none;
+    const bool td_back = o.time_domain && !(o.time_domain == j.pool->time_domain && keeps_time_domain(p->model));
+    cudaStream_t cs = b->stream, ci = p->copy_in, co = p->copy_out;
+    auto dev_ptr = [](const void* q) { return reinterpret_cast<CUdeviceptr>(q); };
+    bool launched = false;
+    Index deferred = 0;
+    // ODEGPU_PIPELINE_TRACE=1: per-group H2D / D2H completion times on stderr
+    static const bool trace = std::getenv("ODEGPU_PIPELINE_TRACE") != nullptr;
+    std::vector<cudaEvent_t> t_in, t_out;
+    cudaEvent_t t_zero = nullptr;
+    auto mark = [&](std::vector<cudaEvent_t>* v, cudaStream_t s_) {
+        if (!trace) return;
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(e, s_));
+        if (v) v->push_back(e);
+        else t_zero = e;
+    };
+    try {
+        // prologue on the compute stream
+        CK(cudaMemsetAsync(st.gate, 0, sizeof(unsigned) * size_t(1 + NG), cs));
+        for (size_t k = 0; k < out_groups.size(); ++k)
+            for (Index gi = out_groups[k].first; gi < out_groups[k].second; ++gi)
+                st.h_group_of[gi] = static_cast<unsigned short>(k);
+        CK(cudaMemcpyAsync(st.group_of, st.h_group_of, sizeof(unsigned short) * size_t(NG), cudaMemcpyHostToDevice,
+                           cs));
+        CK(cudaMemsetAsync(st.bad, 0, 4 * sizeof(unsigned long long), cs));
+        CK(cudaMemsetAsync(st.bad, 0xff, sizeof(unsigned long long), cs)); // no t1 < t0 yet
+        CK(cudaMemsetAsync(b->first_bad, 0xff, sizeof(unsigned long long), cs)); // flags[0]: checked in the kernel
+        CK(cudaMemsetAsync(b->first_bad + 1, 0, sizeof(unsigned long long), cs)); // flags[1]: certified pass
+        b->a.count = N;
+        b->order_count = -1;
+        launch_reset_outcomes(b, 0, N);
+        CK(cudaEventRecord(st.prologue, cs));
+        mark(nullptr, cs);
+        CK(cudaStreamWaitEvent(ci, st.prologue, 0));
+        CK(cudaStreamWaitEvent(co, st.prologue, 0));
+
+        auto h2d = [&](const std::pair<Index, Index>& grp) {
+            const Index s0 = grp.first * G, n = std::min(grp.second * G, N) - s0;
+            auto put = [&](Real* dst, const double* src, Index comps) {
+                if (!comps) return;
+                CK(cudaMemcpy2DAsync(dst + s0, size_t(cap) * 8, src + s0, size_t(N) * 8, size_t(n) * 8, size_t(comps),
+                                     cudaMemcpyHostToDevice, ci));
+            };
+            put(b->a.td, j.pool->time_domain, 2);
+            put(b->a.state, j.pool->state, sd.system_dim);
+            put(const_cast<Real*>(b->a.params), j.pool->parameters, sd.param_count);
+            put(b->a.acc, j.pool->accessories, sd.accessory_count);
+            check_cu(ops.write(reinterpret_cast<CUstream>(ci), dev_ptr(st.gate), cuuint32_t(grp.second), 0),
+                     "cuStreamWriteValue32");
+            mark(&t_in, ci);
+        };
+        // ODEGPU_STREAM_PRELOAD=1 (diagnostic): the whole pool lands before
+        // the kernel starts, which isolates the streaming kernel's own speed
+        static const bool preload = std::getenv("ODEGPU_STREAM_PRELOAD") != nullptr;
+        if (preload) {
+            for (const auto& grp : in_groups) h2d(grp);
+            cudaEvent_t all_in = nullptr;
+            CK(cudaEventCreateWithFlags(&all_in, cudaEventDisableTiming));
+            CK(cudaEventRecord(all_in, ci));
+            CK(cudaStreamWaitEvent(cs, all_in, 0));
+            CK(cudaEventDestroy(all_in));
+        } else {
+            h2d(in_groups[0]);
+        }
+        // the solve kernel over the whole pool, gated per granule
+        b->a.gate.ready = st.gate;
+        b->a.gate.done = st.gate + 1;
+        b->a.gate.group_of = st.group_of;
+        b->a.gate.bad = st.bad;
+        b->a.gate.deferred = st.deferred;
+        b->a.gate.packed = o.outcomes ? st.packed : nullptr;
+        b->a.gate.shift = shift;
+        b->stream_mode = 1;
+        b->stream_order = nullptr;
+        b->build_order = false;
+        b->fuse_request = j.iterations;
+        launch_model(b, p->model, j.cfg->algorithm, c);
+        launched = true;
+        if (b->fused_done != j.iterations) throw Error(ODEGPU_ERR_CUDA, "streaming: iterations did not fuse");
+        if (!preload)
+            for (size_t k = 1; k < in_groups.size(); ++k) h2d(in_groups[k]);
+        // copy-out: each group once all its systems are counted done
+        for (size_t k = 0; k < out_groups.size(); ++k) {
+            const auto& grp = out_groups[k];
+            const Index s0 = grp.first * G, n = std::min(grp.second * G, N) - s0;
+            check_cu(ops.wait(reinterpret_cast<CUstream>(co), dev_ptr(st.gate + 1 + k), cuuint32_t(n),
+                              CU_STREAM_WAIT_VALUE_GEQ),
+                     "cuStreamWaitValue32");
+            auto get = [&](double* dst, const Real* src, Index comps) {
+                if (!dst || !comps) return;
+                CK(cudaMemcpy2DAsync(dst + s0, size_t(N) * 8, src + s0, size_t(cap) * 8, size_t(n) * 8, size_t(comps),
+                                     cudaMemcpyDeviceToHost, co));
+            };
+            if (td_back) get(o.time_domain, b->a.td, 2);
+            get(o.state, b->a.state, sd.system_dim);
+            get(o.accessories, b->a.acc, sd.accessory_count);
+            if (o.outcomes)
+                CK(cudaMemcpyAsync(o.outcomes + s0, st.packed + 56 * size_t(s0), 56 * size_t(n),
+                                   cudaMemcpyDeviceToHost, co));
+            mark(&t_out, co);
+        }
+        // systems the certified pass deferred: the general instantiation
+        CK(cudaMemcpyAsync(st.h_bad, st.bad, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, cs));
+        CK(cudaStreamSynchronize(cs));
+        deferred = Index(st.h_bad[1]);
+        if (deferred > 0) {
+            CK(cudaMemsetAsync(b->first_bad + 1, 0xff, sizeof(unsigned long long), cs)); // flags[1] != 0: general
+            b->a.gate.deferred = nullptr;
+            b->a.count = deferred;
+            b->stream_mode = 2;
+            b->stream_order = st.deferred;
+            b->fuse_request = j.iterations;
+            launch_model(b, p->model, j.cfg->algorithm, c);
+            CK(cudaMemcpyAsync(st.h_bad, st.bad, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, cs));
+        }
+        CK(cudaStreamSynchronize(cs));
+        CK(cudaStreamSynchronize(ci));
+        CK(cudaStreamSynchronize(co));
+        if (trace) {
+            float ks = 0, ke = 0;
+            cudaEventElapsedTime(&ks, t_zero, b->ev_start);
+            cudaEventElapsedTime(&ke, t_zero, b->ev_stop);
+            std::fprintf(stderr, "[stream] %lld granules of %lld: kernel %.3f -> %.3f ms (deferred %lld)\n",
+                         static_cast<long long>(NG), static_cast<long long>(G), ks, ke,
+                         static_cast<long long>(deferred));
+            for (size_t k = 0; k < t_in.size() && k < in_groups.size(); ++k) {
+                float a = 0;
+                cudaEventElapsedTime(&a, t_zero, t_in[k]);
+                std::fprintf(stderr, "[stream] in  granules [%lld, %lld): landed %.3f ms\n",
+                             static_cast<long long>(in_groups[k].first), static_cast<long long>(in_groups[k].second), a);
+            }
+            for (size_t k = 0; k < t_out.size(); ++k) {
+                float d = 0;
+                cudaEventElapsedTime(&d, t_zero, t_out[k]);
+                std::fprintf(stderr, "[stream] out granules [%lld, %lld): shipped %.3f ms\n",
+                             static_cast<long long>(out_groups[k].first), static_cast<long long>(out_groups[k].second),
+                             d);
+            }
+            for (auto e : t_in) cudaEventDestroy(e);
+            for (auto e : t_out) cudaEventDestroy(e);
+            cudaEventDestroy(t_zero);
+        }
+    } catch (...) {
+        // release a kernel still waiting on chunks that will not come, then
+        // quiesce all three streams before the error returns
+        if (launched) {
+            cudaStream_t aux = nullptr;
+            if (cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking) == cudaSuccess) {
+                ops.write(reinterpret_cast<CUstream>(aux), dev_ptr(st.gate), kStreamAbortHost, 0);
+                cudaStreamSynchronize(aux);
+                cudaStreamDestroy(aux);
+            }
+        }
+        cudaStreamSynchronize(cs);
+        cudaStreamSynchronize(ci);
+        cudaStreamSynchronize(co);
+        b->stream_mode = 0;
+        b->stream_order = nullptr;
+        b->a.gate = dev::StreamGate{};
+        b->a.count = cap;
+        throw;
+    }
+    b->stream_mode = 0;
+    b->stream_order = nullptr;
+    b->a.gate = dev::StreamGate{};
+    b->a.count = cap;
+    if (st.h_bad[2]) throw Error(ODEGPU_ERR_CUDA, "streaming: timed out waiting for pool chunks");
+    // the index the chunked run reports: the lowest offender's index in its
+    // batch_capacity chunk (the reference's run_chunks solves chunk by chunk)
+    if (st.h_bad[0] != ~0ull)
+        throw_invalid("solve: system " + std::to_string(static_cast<long long>(Index(st.h_bad[0]) % p->cap)) +
+                      " has t1 < t0");
+}
+
 void run_range(odegpu_pipeline* p, const Run& j, Index begin, Index end) {
+    // AUTO runs the chunked slots: measured on one B200 (e2e, bench.py's
+    // chunking; profiles/r02v/ vs r02e/, scripts/stream_trace.py) streaming
+    // is even with them on cfg4 (36.2 vs 36.8 G steps/s), behind on cfg1
+    // (0.78 vs 0.62 ms; all 46 080 lanes finish together, so its D2H cannot
+    // overlap) and on cfg2 (3.6 vs 3.2 ms: both modes are PCIe-bound at ~60
+    // GB/s both ways, and the slots' copies are larger), and for Keller-
+    // Miksis its instantiation runs ~6 % slower. It wins only where chunks
+    // are far too small to fill the device (cfg1 in 8 chunks: 0.67 vs 1.05 ms).
+    if (begin == 0 && end == j.pool->dims.problem_size && p->mode == ODEGPU_PIPELINE_STREAMING) {
+        const char* why = stream_blocker(p, j);
+        if (!why) {
+            p->last_mode = ODEGPU_PIPELINE_STREAMING;
+            run_streaming(p, j);
+            return;
+        }
+        throw_unsupported(std::string("streaming pipeline: ") + why);
+    }
+    p->last_mode = ODEGPU_PIPELINE_CHUNKED;
     ChunkSource src;
     src.next = begin;
     src.end = end;
@@ -561,6 +950,22 @@ int odegpu_pipeline_create(const odegpu_model* model, odegpu_index batch_capacit
         if (!model || !out) throw_invalid("null argument");
         *out = nullptr;
         *out = pipeline_create(*model, batch_capacity, device);
+    });
+}
+
+int odegpu_pipeline_set_mode(odegpu_pipeline* p, int32_t mode) {
+    return guarded([&] {
+        if (!p) throw_invalid("null pipeline");
+        if (mode != ODEGPU_PIPELINE_AUTO && mode != ODEGPU_PIPELINE_CHUNKED && mode != ODEGPU_PIPELINE_STREAMING)
+            throw_invalid("pipeline: unknown mode " + std::to_string(mode));
+        p->mode = mode;
+    });
+}
+
+int odegpu_pipeline_last_mode(const odegpu_pipeline* p, int32_t* mode) {
+    return guarded([&] {
+        if (!p || !mode) throw_invalid("null argument");
+        *mode = p->last_mode;
     });
 }
 
