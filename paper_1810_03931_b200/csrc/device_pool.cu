@@ -451,8 +451,13 @@ int odegpu_device_pool_solve(odegpu_device_pool* p, const odegpu_model* model, c
             throw_invalid("solve_pool: definition and pool dimensions disagree");
         const Index N = p->dims.problem_size;
         const Index cap = std::min<Index>(batch_capacity, N);
+        // ODEGPU_POOL_TRACE=1: per-chunk timeline and host phases on stderr
+        static const bool trace = std::getenv("ODEGPU_POOL_TRACE") != nullptr;
+        const auto h0 = std::chrono::steady_clock::now();
+        auto host_ms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count(); };
         DeviceGuard g(p->device);
         CK(cudaStreamSynchronize(p->stream));
+        if (trace) std::fprintf(stderr, "[pool] host: entry sync %.3f ms\n", host_ms());
         // the working set: two batches (chunk k+1 gathers and launches while
         // chunk k's kernel drains, on another stream) and the permutation
         if (p->batch_cap != cap || p->batch_model.id != model->id || !p->batch[0]) {
@@ -514,6 +519,7 @@ int odegpu_device_pool_solve(odegpu_device_pool* p, const odegpu_model* model, c
         CK(cudaFreeAsync(d_bad, p->stream));
         CK(cudaStreamSynchronize(p->stream));
         if (bad != ~0ull) throw_invalid("solve: system " + std::to_string(static_cast<long long>(bad)) + " has t1 < t0");
+        if (trace) std::fprintf(stderr, "[pool] host: order + time check %.3f ms\n", host_ms());
 
         const dev::Controls c = prepare_solve(p->batch[0]->dims, model, cfg, ode, ev);
         const PoolOutcomes po{p->final_t, p->smallest, p->reason, p->accepted, p->rejected, p->detections,
@@ -527,8 +533,6 @@ int odegpu_device_pool_solve(odegpu_device_pool* p, const odegpu_model* model, c
                     if (e[i]) cudaEventDestroy(e[i]);
             }
         } guard{done};
-        // ODEGPU_POOL_TRACE=1: per-chunk timeline on stderr
-        static const bool trace = std::getenv("ODEGPU_POOL_TRACE") != nullptr;
         std::vector<cudaEvent_t> tev;
         auto mark = [&](cudaStream_t st) {
             if (!trace) return;
@@ -572,7 +576,9 @@ int odegpu_device_pool_solve(odegpu_device_pool* p, const odegpu_model* model, c
             mark(b->stream);
             start += n;
         }
+        if (trace) std::fprintf(stderr, "[pool] host: chunks enqueued %.3f ms\n", host_ms());
         for (odegpu_batch* b : p->batch) CK(cudaStreamSynchronize(b->stream));
+        if (trace) std::fprintf(stderr, "[pool] host: done %.3f ms\n", host_ms());
         if (trace) {
             for (std::size_t i = 1; i + 1 < tev.size(); i += 2) {
                 float a = 0, d = 0;

@@ -104,3 +104,19 @@ def test_two_rank_slices_reproduce_single_process_run():
     assert np.all(owner >= 0)
     assert np.array_equal(y2.reshape(-1).view(np.uint64), full2["y"].view(np.uint64))
     assert np.array_equal(s2, full2["outcomes"]["accepted_steps"])
+
+
+def test_block_owner_deals_equal_shares_without_grid_resonance():
+    """bench.py's strong-scaling owners: every round of `world` blocks is a
+    permutation of the ranks (equal block counts), and the rotation breaks
+    the fixed rank-to-column pattern of plain block-cyclic ownership."""
+    import bench
+
+    for world in (2, 3, 4, 8):
+        own = bench.block_owner(1000 * world + 5, world)
+        for r0 in range(0, 1000 * world, world):
+            assert sorted(own[r0:r0 + world]) == list(range(world))
+        # blocks 4 apart (one 4096-wide grid row of 1024-blocks) do not all
+        # land on one rank, as they would with own = b % world for world = 4, 8
+        row_start = own[0::4][:200]
+        assert len(set(row_start.tolist())) == world
