@@ -58,6 +58,12 @@ def main():
     check("cfg4", wls.cfg4().strided(2048), 3)
     check("cfg3_knife_edges", wls.cfg3().subset(np.array(KNIFE_EDGES["cfg3"])), 1)
     check("cfg5_knife_edges", wls.cfg5(24).subset(np.array(KNIFE_EDGES["cfg5"])), 1)
+    # off-grid inputs (tests/test_gpu_random_parity.py's generator: random
+    # parameters, time domains, states, tolerances, initial steps, stop counts)
+    from test_gpu_random_parity import make
+
+    for case in ("duffing_event", "duffing_accessory", "duffing_rk4", "valve", "bubble"):
+        check(f"random_{case}", make(case, 7000 + len(case)).strided(512), 2)
 
 
 if __name__ == "__main__":

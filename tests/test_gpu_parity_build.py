@@ -4,7 +4,8 @@ reference solver BIT FOR BIT: time domains, states, accessories and every
 outcome field of every system after every iteration, on strided samples of
 all four configs and on the full-grid systems where the fast build's
 rounding flips a knife-edge accept / reject decision (the full-size runs:
-profiles/r02b/parity_fullsize_parity_build.jsonl)."""
+profiles/r02b/parity_fullsize_parity_build.jsonl), and on seeded random
+off-grid inputs of every built-in model over two iterations."""
 import json
 import os
 import subprocess
@@ -30,7 +31,9 @@ def cases():
     return {d["case"]: d for d in (json.loads(l) for l in r.stdout.splitlines() if l.startswith("{"))}
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg3_knife_edges", "cfg5_knife_edges"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg3_knife_edges", "cfg5_knife_edges",
+                                  "random_duffing_event", "random_duffing_accessory", "random_duffing_rk4",
+                                  "random_valve", "random_bubble"])
 def test_parity_build_bitwise_reference(cases, name):
     c = cases[name]
     assert c["td"] == 0 and c["y"] == 0 and c["acc"] == 0, c
