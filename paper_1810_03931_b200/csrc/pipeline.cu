@@ -12,6 +12,7 @@
 #include <cstring>
 #include <exception>
 #include <mutex>
+#include <span>
 #include <string>
 #include <thread>
 #include <vector>
@@ -202,8 +203,13 @@ struct odegpu_pipeline {
     Index cap = 0;
     int device = 0;
     Index rec_capacity = 0; // recorded iterations the staging can hold
-    static constexpr int kSlots = 4; // chunks in flight: copy-in, compute (two), copy-out
-    odegpu::detail::Slot slots[kSlots];
+    // chunks in flight (device batches + pinned staging): copy-in, compute
+    // (two), copy-out and the ones whose H2D runs ahead. 6 measured best on
+    // one B200 (e2e, bench chunking: cfg2 3.06 ms vs 3.19 with 4 and 3.09
+    // with 8; cfg1 / cfg4 / cfg5 flat); ODEGPU_PIPELINE_SLOTS overrides it
+    static constexpr int kMaxSlots = 8;
+    int n_slots = 6;
+    odegpu::detail::Slot slots[kMaxSlots];
     cudaStream_t copy_in = nullptr, copy_out = nullptr;
     std::vector<odegpu_outcome> packed;
     unsigned long long* d_tally = nullptr; // device scan tally (kTallySlots counters)
@@ -248,12 +254,14 @@ odegpu_pipeline* pipeline_create(const odegpu_model& model, Index capacity, int 
         p->sd = dims_of(model);
         p->cap = capacity;
         p->device = device;
+        if (const char* e = std::getenv("ODEGPU_PIPELINE_SLOTS"))
+            p->n_slots = std::clamp(std::atoi(e), 3, odegpu_pipeline::kMaxSlots);
         DeviceGuard g(device);
         const auto& sd = p->sd;
         const odegpu_batch_dims bd{capacity, sd.system_dim, sd.param_count, sd.event_count, sd.accessory_count};
         CK(cudaStreamCreateWithFlags(&p->copy_in, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&p->copy_out, cudaStreamNonBlocking));
-        for (auto& s : p->slots) {
+        for (auto& s : std::span(p->slots, size_t(p->n_slots))) {
             s.batch = batch_create(bd, device);
             for (cudaEvent_t* e : {&s.loaded, &s.computed, &s.done})
                 CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -277,7 +285,7 @@ void reserve_records(odegpu_pipeline* p, Index n_rec, uint32_t mask) {
     if (n_rec <= p->rec_capacity) return;
     const auto& sd = p->sd;
     const Index cap = p->cap;
-    for (auto& s : p->slots) {
+    for (auto& s : std::span(p->slots, size_t(p->n_slots))) {
         for (double* q : {s.rec_td, s.rec_y, s.rec_acc})
             if (q) cudaFreeHost(q);
         s.rec_td = s.rec_y = s.rec_acc = nullptr;
@@ -334,7 +342,7 @@ void run_chunks(odegpu_pipeline* p, const Run& j, ChunkSource& src) {
     unsigned long long* tally = j.tally ? p->d_tally : nullptr;
     // zeroed on the copy-in stream: every chunk's kernels wait for its H2D
     if (tally) CK(cudaMemsetAsync(tally, 0, dev::kTallySlots * sizeof(unsigned long long), p->copy_in));
-    for (auto& s : p->slots) s.batch->a.tally = tally;
+    for (auto& s : std::span(p->slots, size_t(p->n_slots))) s.batch->a.tally = tally;
     if (n_rec > 0) {
         // (re)allocate when the mask needs arrays the staging lacks
         const Slot& s0 = p->slots[0];
@@ -404,13 +412,13 @@ void run_chunks(odegpu_pipeline* p, const Run& j, ChunkSource& src) {
         CK(cudaEventRecord(e, st));
         tev.push_back(e);
     };
-    // Three-stage pipeline over kSlots device batches: chunk k's H2D runs on
+    // Three-stage pipeline over n_slots device batches: chunk k's H2D runs on
     // the copy-in stream, its kernels on the slot batch's stream (after the
     // H2D event), its D2H on the copy-out stream (after the kernels' event),
     // so H2D(k+1), the kernels of k and D2H(k-1) overlap (PCIe is full
     // duplex: 55 GB/s each way measured on the B200 box, 99 GB/s both). A
     // slot is refilled only after its previous chunk was drained on the host.
-    constexpr int kSlots = odegpu_pipeline::kSlots;
+    const int kSlots = p->n_slots;
     int k = 0;
     try {
         Index start = 0, n = 0;
@@ -533,18 +541,18 @@ void run_chunks(odegpu_pipeline* p, const Run& j, ChunkSource& src) {
             t.start_time_not_advanced += Index(h[dev::kTallyStartNotAdvanced]);
             t.nonfinite_systems += Index(h[dev::kTallyNonfinite]);
         }
-        for (auto& s : p->slots) s.batch->a.tally = nullptr;
+        for (auto& s : std::span(p->slots, size_t(p->n_slots))) s.batch->a.tally = nullptr;
     } catch (...) {
         // Quiesce every stream of the pipeline before handing control back:
         // queued D2H copies could otherwise still write into the caller's
         // page-locked arrays after the error returns, and a later run could
         // reuse a slot whose old copies are pending.
-        for (auto& s : p->slots) s.batch->a.tally = nullptr;
+        for (auto& s : std::span(p->slots, size_t(p->n_slots))) s.batch->a.tally = nullptr;
         cudaStreamSynchronize(p->copy_in);
-        for (auto& s : p->slots)
+        for (auto& s : std::span(p->slots, size_t(p->n_slots)))
             if (s.batch) cudaStreamSynchronize(s.batch->stream);
         cudaStreamSynchronize(p->copy_out);
-        for (auto& s : p->slots) s.busy = false;
+        for (auto& s : std::span(p->slots, size_t(p->n_slots))) s.busy = false;
         throw;
     }
 }

@@ -19,7 +19,8 @@ for name in sys.argv[1:] or ["cfg2"]:
             None if no_oc else pinned(np.zeros(n, dtype=abi.OUTCOME_DTYPE)))
     cfg = pkg.SolverConfig(wl.algorithm, wl.dt)
     for mode in modes:
-        chunks = 8 if wl.instr_per_step < 500 else 16
+        # bench.py's chunking
+        chunks = int(os.environ.get("CHUNKS", 0)) or int(min(max(round(n / 65536), 2), 16 if wl.instr_per_step > 500 else 8))
         pipe = Pipeline(wl.model, -(-n // chunks), 0, mode=mode)
         pipe.run(pool, cfg, 1, out_arrays=outs)
         best = 1e9
