@@ -56,21 +56,18 @@ struct Controls {
 /// pool arrives in granules of 2^shift systems while the kernel runs. A lane
 /// takes up system s only once *ready > s >> shift (the copy-in stream
 /// bumps it after each granule group's H2D) and counts s when it is
-/// finished, which releases its group's D2H on the copy-out stream. bad: [0] lowest index with t1 < t0 (~0: none),
-/// [1] systems deferred to the general-trig pass, [2] nonzero: aborted by
-/// the host or timed out. A finished system is counted into
-/// done[group_of[granule]]: one counter (and one stream wait) per copy-out
-/// group. deferred, when non-null (the certified first
-/// pass): systems whose trig arguments exceed the certified range, appended
-/// instead of integrated. packed: every finished system's outcome record in
-/// the reference's 56-byte AoS layout (odegpu_outcome = SystemOutcome,
-/// driver.hpp:34-42), so the D2H ships records without a packing pass.
+/// finished, into done[group_of[granule]] — one counter (and one stream
+/// wait) per copy-out group — which releases that group's D2H on the
+/// copy-out stream. bad: [0] lowest index with t1 < t0 (~0: none), [2]
+/// nonzero: aborted by the host or timed out. packed: every finished
+/// system's outcome record in the reference's 56-byte AoS layout
+/// (odegpu_outcome = SystemOutcome, driver.hpp:34-42), so the D2H ships
+/// records without a packing pass.
 struct StreamGate {
     const unsigned* ready = nullptr;
     unsigned* done = nullptr;             // per copy-out group (group_of[granule])
     const unsigned short* group_of = nullptr;
     unsigned long long* bad = nullptr;
-    unsigned* deferred = nullptr;
     unsigned char* packed = nullptr;
     unsigned shift = 0;
 };
@@ -878,14 +875,9 @@ constexpr std::size_t solve_smem_bytes() {
 /// without another trip through the state machine. Only detections, stops
 /// and system ends go back through PREPARE.
 ///
-/// Bound: in the certified instantiation, the general model whose
-/// trig_argument_bound a streaming run checks per system as it takes it up
-/// (StreamGate::deferred); void otherwise.
-///
 /// STREAM: the streaming-pool instantiation (BatchArrays::gate); the
 /// others carry none of its code.
-template <class H, Algorithm ALG, int BLOCK, class Pol = EffectivePolicy<H>, bool LOG = false, class Bound = void,
-          bool STREAM = false>
+template <class H, Algorithm ALG, int BLOCK, class Pol = EffectivePolicy<H>, bool LOG = false, bool STREAM = false>
 __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, const Controls& c) {
     constexpr int N = H::kSystemDim;
     constexpr int NP = H::kParamCount, NA = H::kAccessoryCount, E = H::kEventCount;
@@ -915,25 +907,17 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
     const Index n = b.n;
     // STREAM: pending counts + the block's landed-granule watermark
     [[maybe_unused]] unsigned* const s_stream = stream_shared<STREAM, BLOCK>();
-    // STREAM: a system's own checks as it is taken up (true: not integrated
-    // — t1 < t0, solve.hpp:159-161, counted done and reported in bad[0]; or,
-    // in the certified instantiation, trig arguments beyond the certified
-    // range: deferred to the general pass). Run on the values the fetch
-    // loads anyway (late) where that is free; before the loads (early) for
-    // models whose parameters live in shared memory, whose register budget
-    // the late form overruns (Keller-Miksis: 16 B of spills).
+    // STREAM: a system's own t1 < t0 check (solve.hpp:159-161) as it is
+    // taken up (true: not integrated, counted done and reported in bad[0]).
+    // Run on the values the fetch loads anyway (late) where that is free;
+    // before the loads (early) for models whose parameters live in shared
+    // memory, whose register budget the late form overran (Keller-Miksis).
     constexpr bool kLateStreamChecks = !Pol::kParamsInShared;
-    [[maybe_unused]] const auto stream_checks = [&](Real t0, Real t1, const Real* p, Index stride, unsigned sys_) {
+    [[maybe_unused]] const auto stream_checks = [&](Real t0, Real t1, unsigned sys_) {
         if (t1 < t0) {
             atomicMin(b.gate.bad, static_cast<unsigned long long>(sys_));
             stream_release(b.gate, sys_);
             return true;
-        }
-        if constexpr (!std::is_void_v<Bound>) {
-            if (b.gate.deferred && !(Bound::trig_argument_bound(t0, t1, p, stride) < kTrigCertifiedLimit)) {
-                b.gate.deferred[atomicAdd(b.gate.bad + 1, 1ull)] = sys_;
-                return true;
-            }
         }
         return false;
     };
@@ -1136,8 +1120,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
                             continue;
                         }
                         if constexpr (!kLateStreamChecks) {
-                            const Real t0 = b.td[sys], t1 = b.td[sys + n];
-                            if (stream_checks(t0, t1, b.params + sys, n, static_cast<unsigned>(sys))) continue;
+                            if (stream_checks(b.td[sys], b.td[sys + n], static_cast<unsigned>(sys))) continue;
                         }
                     }
                     // solve.hpp:98 (never in a streaming run: it resets every outcome first)
@@ -1157,7 +1140,7 @@ __device__ __forceinline__ void solve_lanes(const H& m, const BatchArrays& b, co
 #pragma unroll
                 for (int i = 0; i < NA; ++i) acc[i] = b.acc[sys + i * n];
                 if constexpr (STREAM && kLateStreamChecks)
-                    if (phase == kFetch && stream_checks(td[0], td[1], prow, 1, static_cast<unsigned>(sys))) continue;
+                    if (phase == kFetch && stream_checks(td[0], td[1], static_cast<unsigned>(sys))) continue;
                 ODEGPU_B(n_acc) = ODEGPU_B(n_rej) = 0u;
                 ODEGPU_C(acc_hi) = ODEGPU_C(rej_hi) = 0u;
                 ODEGPU_C(n_det) = ODEGPU_C(n_secf) = 0ull;
@@ -1578,21 +1561,24 @@ __global__ void trig_certificate_kernel(BatchArrays b, unsigned long long* flags
 /// (driver.hpp:186-206) it costs nothing when nobody observes.
 ///
 /// STREAM: the streaming-pool instantiation (odegpu_pipeline STREAMING):
-/// lanes wait on the chunk gate, check t1 < t0 and (certified path) the
-/// trig bound per system, and write packed records and chunk counts.
+/// lanes wait on the granule gate, check t1 < t0 per system, and write
+/// packed records and per-group counts. A streaming run takes the general
+/// trig path (flags[1] != 0): the certificate needs every system before the
+/// launch, and a second launch for systems a certified pass would have to
+/// leave out could wait behind the copy-out stream's value waits.
 template <class H, Algorithm ALG, int BLOCK, int MIN_BLOCKS, bool LOG = false, bool STREAM = false>
 __global__ void __launch_bounds__(BLOCK, MIN_BLOCKS)
     guarded_solve_kernel(H model, BatchArrays b, Controls c, const unsigned long long* flags) {
     if (flags[0] != ~0ull) return;
     dmath::init_shared_tables();
-    if constexpr (TrigCertifiable<H>) {
+    if constexpr (TrigCertifiable<H> && !STREAM) {
         if (flags[1] == 0) {
-            solve_lanes<typename H::certified_hooks, ALG, BLOCK, EffectivePolicy<H>, LOG, H, STREAM>(
+            solve_lanes<typename H::certified_hooks, ALG, BLOCK, EffectivePolicy<H>, LOG, STREAM>(
                 typename H::certified_hooks{}, b, c);
             return;
         }
     }
-    solve_lanes<H, ALG, BLOCK, EffectivePolicy<H>, LOG, void, STREAM>(model, b, c);
+    solve_lanes<H, ALG, BLOCK, EffectivePolicy<H>, LOG, STREAM>(model, b, c);
 }
 
 /// Kernel controls from the C-ABI structs (materialised once per solve,

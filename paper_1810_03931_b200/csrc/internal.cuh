@@ -103,11 +103,10 @@ struct odegpu_batch {
     odegpu::Index fused_done = 1;
     unsigned long long* trial_steps = nullptr; // device: trial steps integrated since the last reset
     void* log_block = nullptr; // detection log (odegpu_batch_set_detection_log), BatchArrays::log_*
-    // streaming pool run (pipeline.cu): 1 = the pass over the arriving
-    // chunks, 2 = the general-trig pass over the systems it deferred; the
-    // launch then skips the certificate pre-pass and fetches in stream_order
+    // streaming pool run (pipeline.cu): nonzero = the launch is the
+    // streaming pass (STREAM instantiation, natural fetch order; the caller
+    // has set both flags, so no certificate pre-pass)
     int stream_mode = 0;
-    const unsigned* stream_order = nullptr;
 };
 
 namespace odegpu::detail {

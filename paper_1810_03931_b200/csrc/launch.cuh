@@ -51,12 +51,14 @@ void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
     // observer path instead of spills)
     const bool log = H::kEventCount > 0 && b->a.log_count != nullptr;
     // streaming pool (pipeline.cu): its own instantiation; the caller has set
-    // both flags and the fetch order, the certificate is checked per system
+    // both flags (general trig path), fetch in natural order
     const bool streaming = b->stream_mode != 0;
     auto kern = guarded_solve_kernel<H, ALG, kBlock, kMin, false, false>;
     if constexpr (H::kEventCount > 0)
         if (log) kern = guarded_solve_kernel<H, ALG, kBlock, (kMin > 1 ? kMin - 1 : 1), true, false>;
-    if (streaming) kern = guarded_solve_kernel<H, ALG, kBlock, kMin, false, true>;
+    // (one block per SM fewer, like the log: the streaming pass runs the
+    // general trig path plus its gate, and stays spill-free)
+    if (streaming) kern = guarded_solve_kernel<H, ALG, kBlock, (kMin > 1 ? kMin - 1 : 1), false, true>;
     const int variant = streaming ? 2 : log ? 1 : 0;
     constexpr std::size_t smem = dev::solve_smem_bytes<H, ALG, kBlock>();
     if constexpr (smem > 48 * 1024) // opt-in above the static limit (per device)
@@ -92,7 +94,7 @@ void launch_one(odegpu_batch* b, const H& hooks, const dev::Controls& c) {
     }();
     const bool cost = !streaming && (b->order_mode == ODEGPU_FETCH_COST ||
                                      (b->order_mode == ODEGPU_FETCH_AUTO && kPolicyCost));
-    b->a.order = streaming ? b->stream_order : (cost && b->order_count == n) ? b->order : nullptr;
+    b->a.order = (!streaming && cost && b->order_count == n) ? b->order : nullptr;
     b->a.cost = (cost && b->build_order) ? b->cost : nullptr; // null until the first order build allocates it
     // fused iterations: the systems of this launch are solved `fused` times
     // in a row (hooks.hpp kFusableIterations; one solve otherwise)

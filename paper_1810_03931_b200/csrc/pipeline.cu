@@ -156,11 +156,10 @@ struct StreamState {
     odegpu_batch* batch = nullptr;
     Index cap = 0;
     unsigned* gate = nullptr;               // [0] chunks landed, [1 + c] systems of chunk c finished
-    unsigned long long* bad = nullptr;      // BatchArrays::stream_bad (4 words)
+    unsigned long long* bad = nullptr;      // StreamGate::bad (4 words)
     unsigned long long* h_bad = nullptr;    // pinned mirror
     unsigned short* group_of = nullptr;     // [kMaxGranules] granule -> copy-out group (device)
     unsigned short* h_group_of = nullptr;   // pinned staging
-    unsigned* deferred = nullptr;           // [cap]
     unsigned char* packed = nullptr;        // [cap] x 56 B
     cudaEvent_t prologue = nullptr;
     void release() {
@@ -168,8 +167,7 @@ struct StreamState {
             cudaStreamSynchronize(batch->stream);
             odegpu_batch_destroy(batch);
         }
-        for (void* q : {static_cast<void*>(gate), static_cast<void*>(bad), static_cast<void*>(deferred),
-                        static_cast<void*>(packed)})
+        for (void* q : {static_cast<void*>(gate), static_cast<void*>(bad), static_cast<void*>(packed)})
             if (q) cudaFree(q);
         if (h_bad) cudaFreeHost(h_bad);
         if (group_of) cudaFree(group_of);
@@ -642,7 +640,6 @@ void stream_reserve(odegpu_pipeline* p, Index N) {
         CK(cudaMallocHost(&st.h_bad, 4 * sizeof(unsigned long long)));
         CK(cudaMalloc(&st.group_of, sizeof(unsigned short) * StreamState::kMaxGranules));
         CK(cudaMallocHost(&st.h_group_of, sizeof(unsigned short) * StreamState::kMaxGranules));
-        CK(cudaMalloc(&st.deferred, sizeof(unsigned) * size_t(N)));
         CK(cudaMalloc(&st.packed, 56 * size_t(N)));
         CK(cudaEventCreateWithFlags(&st.prologue, cudaEventDisableTiming));
     } catch (...) {
@@ -696,9 +693,13 @@ std::vector<std::pair<Index, Index>> granule_groups(Index ng, bool small_last) {
 ///                   end (cuStreamWriteValue32), group after group
 ///   copy-out:       [prologue] -> for a granule group: wait gate[1 + g] >=
 ///                   granule size for each g (cuStreamWaitValue32) -> D2H
-/// Systems the certified kernel defers (trig arguments beyond the certified
-/// range) run afterwards in a second launch of the general instantiation
-/// over the deferred list; their granules' D2H wait for it.
+/// The kernel takes the general trig path: the trig certificate needs every
+/// system before the launch, and a second launch for systems a certified
+/// pass left out would be queued after the copy-out stream's value waits
+/// that depend on it — under false serialization of streams (shared
+/// hardware queues; compute-sanitizer serialises them outright) a deadlock.
+/// A first pass whose input never lands gives up after kStreamTimeoutNs and
+/// counts every system done, so no wait is left hanging.
 void run_streaming(odegpu_pipeline* p, const Run& j) {
     const odegpu_pool_dims& pd = j.pool->dims;
     const odegpu_system_dims& sd = p->sd;
@@ -720,7 +721,6 @@ void run_streaming(odegpu_pipeline* p, const Run& j) {
     cudaStream_t cs = b->stream, ci = p->copy_in, co = p->copy_out;
     auto dev_ptr = [](const void* q) { return reinterpret_cast<CUdeviceptr>(q); };
     bool launched = false;
-    Index deferred = 0;
     // ODEGPU_PIPELINE_TRACE=1: per-group H2D / D2H completion times on stderr
     static const bool trace = std::getenv("ODEGPU_PIPELINE_TRACE") != nullptr;
     std::vector<cudaEvent_t> t_in, t_out;
@@ -744,7 +744,7 @@ void run_streaming(odegpu_pipeline* p, const Run& j) {
         CK(cudaMemsetAsync(st.bad, 0, 4 * sizeof(unsigned long long), cs));
         CK(cudaMemsetAsync(st.bad, 0xff, sizeof(unsigned long long), cs)); // no t1 < t0 yet
         CK(cudaMemsetAsync(b->first_bad, 0xff, sizeof(unsigned long long), cs)); // flags[0]: checked in the kernel
-        CK(cudaMemsetAsync(b->first_bad + 1, 0, sizeof(unsigned long long), cs)); // flags[1]: certified pass
+        CK(cudaMemsetAsync(b->first_bad + 1, 0xff, sizeof(unsigned long long), cs)); // flags[1]: general trig
         b->a.count = N;
         b->order_count = -1;
         launch_reset_outcomes(b, 0, N);
@@ -786,11 +786,9 @@ void run_streaming(odegpu_pipeline* p, const Run& j) {
         b->a.gate.done = st.gate + 1;
         b->a.gate.group_of = st.group_of;
         b->a.gate.bad = st.bad;
-        b->a.gate.deferred = st.deferred;
         b->a.gate.packed = o.outcomes ? st.packed : nullptr;
         b->a.gate.shift = shift;
         b->stream_mode = 1;
-        b->stream_order = nullptr;
         b->build_order = false;
         b->fuse_request = j.iterations;
         launch_model(b, p->model, j.cfg->algorithm, c);
@@ -818,20 +816,7 @@ void run_streaming(odegpu_pipeline* p, const Run& j) {
                                    cudaMemcpyDeviceToHost, co));
             mark(&t_out, co);
         }
-        // systems the certified pass deferred: the general instantiation
         CK(cudaMemcpyAsync(st.h_bad, st.bad, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, cs));
-        CK(cudaStreamSynchronize(cs));
-        deferred = Index(st.h_bad[1]);
-        if (deferred > 0) {
-            CK(cudaMemsetAsync(b->first_bad + 1, 0xff, sizeof(unsigned long long), cs)); // flags[1] != 0: general
-            b->a.gate.deferred = nullptr;
-            b->a.count = deferred;
-            b->stream_mode = 2;
-            b->stream_order = st.deferred;
-            b->fuse_request = j.iterations;
-            launch_model(b, p->model, j.cfg->algorithm, c);
-            CK(cudaMemcpyAsync(st.h_bad, st.bad, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, cs));
-        }
         CK(cudaStreamSynchronize(cs));
         CK(cudaStreamSynchronize(ci));
         CK(cudaStreamSynchronize(co));
@@ -839,9 +824,8 @@ void run_streaming(odegpu_pipeline* p, const Run& j) {
             float ks = 0, ke = 0;
             cudaEventElapsedTime(&ks, t_zero, b->ev_start);
             cudaEventElapsedTime(&ke, t_zero, b->ev_stop);
-            std::fprintf(stderr, "[stream] %lld granules of %lld: kernel %.3f -> %.3f ms (deferred %lld)\n",
-                         static_cast<long long>(NG), static_cast<long long>(G), ks, ke,
-                         static_cast<long long>(deferred));
+            std::fprintf(stderr, "[stream] %lld granules of %lld: kernel %.3f -> %.3f ms\n",
+                         static_cast<long long>(NG), static_cast<long long>(G), ks, ke);
             for (size_t k = 0; k < t_in.size() && k < in_groups.size(); ++k) {
                 float a = 0;
                 cudaEventElapsedTime(&a, t_zero, t_in[k]);
@@ -874,13 +858,11 @@ void run_streaming(odegpu_pipeline* p, const Run& j) {
         cudaStreamSynchronize(ci);
         cudaStreamSynchronize(co);
         b->stream_mode = 0;
-        b->stream_order = nullptr;
         b->a.gate = dev::StreamGate{};
         b->a.count = cap;
         throw;
     }
     b->stream_mode = 0;
-    b->stream_order = nullptr;
     b->a.gate = dev::StreamGate{};
     b->a.count = cap;
     if (st.h_bad[2]) throw Error(ODEGPU_ERR_CUDA, "streaming: timed out waiting for pool chunks");

@@ -92,9 +92,10 @@ def test_streaming_in_place_fused_iterations(cfg, count, its, monkeypatch):
     pipe.close()
 
 
-def test_streaming_defers_uncertified_systems(monkeypatch):
-    """Systems whose trig arguments exceed the certified range are deferred
-    by the certified pass and integrated by the general one: bitwise the
+def test_streaming_integrates_systems_beyond_the_trig_certificate(monkeypatch):
+    """The streaming pass takes the general trig path (the certificate would
+    need every system before the launch): systems whose trig arguments need
+    Payne-Hanek reduction are integrated like the rest — bitwise the
     resident batch (whose certificate then fails for the whole batch)."""
     monkeypatch.setenv("ODEGPU_STREAM_CHUNK", "64")
     wl = workloads.cfg2().strided(1000)
