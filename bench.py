@@ -17,10 +17,12 @@ continues from the previous step's end point (one collapse per system).
   around all K steps (plus the per-step device outcome tally), bracketed by a
   barrier + synchronize; max over ranks. The pool (3.3 GB at 2^24) is larger
   than L2, so no flush is needed between steps.
-* fetch order: lanes take systems longest first by their cost in the
-  PREVIOUS iteration (AUTO policy) — information a real scan has. cfg2 cannot
-  iterate in place (the reference's secant Zeno loop): every
-  step restarts from the initial conditions and runs in natural order.
+* fetch order (AUTO policy): Keller-Miksis pools in index order (the cost
+  order measured even at 2^24 and doubled DRAM traffic), the valve longest
+  first by each system's cost in the PREVIOUS iteration — information a real
+  scan has. cfg2 cannot iterate in place (the reference's secant Zeno loop,
+  DESIGN.md §4): every step restarts from the initial conditions and runs in
+  natural order.
 * e2e: the same metric through the C ABI with host (pinned) buffers — the
   chunked pool pipeline (odegpu_pipeline_run): per step H2D of the pool, one
   in-place iteration, D2H of the end points and outcome records into the
@@ -135,6 +137,11 @@ def block_owner(n_blocks: int, world: int) -> np.ndarray:
     b = np.arange(n_blocks, dtype=np.uint64)
     off = (((b // np.uint64(world)) * np.uint64(0x9E3779B1)) >> np.uint64(11)) % np.uint64(world)
     return ((b + off) % np.uint64(world)).astype(np.int64)
+
+
+def keller_miksis(wl) -> bool:
+    """Keller-Miksis pools take their systems in index order under AUTO."""
+    return wl.model.to_c().id in (abi.MODEL_KELLER_MIKSIS, abi.MODEL_BUBBLE_COLLAPSE)
 
 
 def in_place(config: str) -> bool:
@@ -450,7 +457,7 @@ def main():
     # ---------------- the same iterations in natural fetch order (outside the
     # timed region): a snapshot of the pool is solved once ordered, once not
     natural = None
-    if ip and wl.algorithm == abi.RKCK45 and not args.no_natural:
+    if ip and wl.algorithm == abi.RKCK45 and not keller_miksis(wl) and not args.no_natural:
         k_nat = min(args.steps, 3)
         snap = pkg.SolverBatch(pkg.make_batch_dims(n, wl.model.dims()), device=device)
         pkg.batch_copy(snap, batch)
@@ -559,8 +566,10 @@ def main():
                        "CUDA events on each rank's batch stream, max over ranks"),
             "trig_path": "certified (branch-free, include/odegpu/trig.hpp)" if certified else "general",
             "fetch_order": ("longest first by each system's RK evaluations in the PREVIOUS iteration (AUTO "
-                            "policy, what an in-place scan knows)") if ip and wl.algorithm == abi.RKCK45 else
-                           "natural (index order)",
+                            "policy, what an in-place scan knows)") if ip and wl.algorithm == abi.RKCK45 and
+                           not keller_miksis(wl) else
+                           "natural (index order; AUTO for Keller-Miksis and fixed-step RK4, "
+                           "csrc/models_keller_miksis.cu)",
             "natural_order": natural,
             "library": os.environ.get("ODEGPU_LIB") or ("parity" if os.environ.get("ODEGPU_BUILD") == "parity"
                                                          else "libodegpu.so (fast build)"),

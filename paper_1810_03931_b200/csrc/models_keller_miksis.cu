@@ -28,15 +28,28 @@ struct KernelPolicy<odegpu::models::KellerMiksisHooks> {
 
 namespace odegpu::detail {
 
+// Keller-Miksis systems are taken up in index order under AUTO. Longest
+// first by the previous iteration (the cost order) measured even at 2^24
+// (bench cfg5: 10.96 vs 10.96 G steps/s) and 2 % behind at 2^20 (cfg3: 9.49
+// vs 9.67; profiles/r02ai/), and it scatters a warp's entry / exit accesses
+// over 32 distant systems: 10.1 GB of DRAM traffic per in-place iteration
+// of the 2^24 pool against 4.7 GB algorithmic (ncu, profiles/r02ag_ncu_summary.md).
+// With ~226 systems per lane at 2^24 and the fused iterations, the end-of-
+// pool tail the order was for is no longer there. -DODEGPU_KM_COST_ORDER=true
+// restores it (tuning).
+#ifndef ODEGPU_KM_COST_ORDER
+#define ODEGPU_KM_COST_ORDER false
+#endif
+
 template <>
 struct LaunchPolicy<models::BubbleCollapseHooks> {
     static constexpr int kMinBlocks = ODEGPU_MB(5);
-    static constexpr bool kCostOrder = true; // step counts spread widely: longest first
+    static constexpr bool kCostOrder = ODEGPU_KM_COST_ORDER;
 };
 template <>
 struct LaunchPolicy<models::KellerMiksisHooks> {
     static constexpr int kMinBlocks = ODEGPU_MB(5);
-    static constexpr bool kCostOrder = true; // step counts spread widely: longest first
+    static constexpr bool kCostOrder = ODEGPU_KM_COST_ORDER;
 };
 
 // 5 resident blocks need 5 x (layout + 1 KB reserved) <= 228 KB of shared

@@ -42,6 +42,8 @@ def test_auto_follows_the_model_policy():
     assert run(wl, abi.FETCH_AUTO, 2)["launches"] == run(wl, abi.FETCH_NATURAL, 2)["launches"]
     wl = workloads.CONFIGS["cfg4"]().strided(4096)  # adaptive valve: cost order
     assert run(wl, abi.FETCH_AUTO, 2)["launches"] == run(wl, abi.FETCH_COST, 2)["launches"]
+    wl = workloads.CONFIGS["cfg3"]().strided(4096)  # Keller-Miksis: index order (models_keller_miksis.cu)
+    assert run(wl, abi.FETCH_AUTO, 2)["launches"] == run(wl, abi.FETCH_NATURAL, 2)["launches"]
 
 
 def test_rejects_unknown_mode():
