@@ -771,15 +771,19 @@ void run_streaming(odegpu_pipeline* p, const Run& j) {
         // ODEGPU_STREAM_PRELOAD=1 (diagnostic): the whole pool lands before
         // the kernel starts, which isolates the streaming kernel's own speed
         static const bool preload = std::getenv("ODEGPU_STREAM_PRELOAD") != nullptr;
+        // Every H2D group is enqueued BEFORE the kernel, so the kernel only
+        // ever waits on work queued ahead of it: were the copy-in and compute
+        // streams falsely serialised (shared hardware queue), the copies
+        // would simply finish first (less overlap, no deadlock). Enqueueing
+        // the ~20 groups takes the host well under a millisecond, while
+        // group 0's copy is already running.
+        for (const auto& grp : in_groups) h2d(grp);
         if (preload) {
-            for (const auto& grp : in_groups) h2d(grp);
             cudaEvent_t all_in = nullptr;
             CK(cudaEventCreateWithFlags(&all_in, cudaEventDisableTiming));
             CK(cudaEventRecord(all_in, ci));
             CK(cudaStreamWaitEvent(cs, all_in, 0));
             CK(cudaEventDestroy(all_in));
-        } else {
-            h2d(in_groups[0]);
         }
         // the solve kernel over the whole pool, gated per granule
         b->a.gate.ready = st.gate;
@@ -794,8 +798,6 @@ void run_streaming(odegpu_pipeline* p, const Run& j) {
         launch_model(b, p->model, j.cfg->algorithm, c);
         launched = true;
         if (b->fused_done != j.iterations) throw Error(ODEGPU_ERR_CUDA, "streaming: iterations did not fuse");
-        if (!preload)
-            for (size_t k = 1; k < in_groups.size(); ++k) h2d(in_groups[k]);
         // copy-out: each group once all its systems are counted done
         for (size_t k = 0; k < out_groups.size(); ++k) {
             const auto& grp = out_groups[k];
