@@ -17,7 +17,9 @@
 #define ODEGPU_SCAN_HPP
 
 #include <array>
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <fstream>
 #include <limits>
@@ -202,6 +204,15 @@ struct Chunk {
 /// `diag`.
 using Rows = std::vector<std::vector<Real>>;
 
+/// ODEGPU_SCAN_TRACE=1: host-side phase times of a scan on stderr.
+inline void scan_trace(const char* what) {
+    static const bool on = std::getenv("ODEGPU_SCAN_TRACE") != nullptr;
+    if (!on) return;
+    static auto t0 = std::chrono::steady_clock::now();
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "[scan] %10.3f ms  %s\n", ms, what);
+}
+
 template <SystemModel D, class OnChunk>
 void run_chunks(const D& def, const ProblemPool& pool, const SolveOptions& opt, Index transient, Index saved,
                 uint32_t record_mask, ScanResult& result, OnChunk&& on_chunk, bool check_start_times = false) {
@@ -239,6 +250,7 @@ void run_chunks(const D& def, const ProblemPool& pool, const SolveOptions& opt, 
     odegpu_scan_tally t{};
     const odegpu_pool_view v = pool.view();
     int rc = 0;
+    scan_trace("run_chunks: start");
     if (opt.devices.size() > 1) {
         rc = odegpu_solve_pool_multi_tallied(&v, &out, &m, &cc.c_cfg, &cc.c_ode, &cc.c_ev, cap, transient + saved,
                                              transient, record_mask | kRecOutcomes, sink, &ctx, opt.devices.data(),
@@ -246,14 +258,18 @@ void run_chunks(const D& def, const ProblemPool& pool, const SolveOptions& opt, 
     } else {
         odegpu_pipeline* pipe = nullptr;
         odegpu::detail::check(odegpu_pipeline_create(&m, cap, opt.devices.empty() ? opt.device : opt.devices[0], &pipe));
+        scan_trace("run_chunks: pipeline created");
         rc = odegpu_pipeline_run_tallied(pipe, &v, &out, &cc.c_cfg, &cc.c_ode, &cc.c_ev, transient + saved, transient,
                                          record_mask | kRecOutcomes, sink, &ctx, &t);
+        scan_trace("run_chunks: pipeline run");
         odegpu_pipeline_destroy(pipe);
+        scan_trace("run_chunks: pipeline destroyed");
     }
     if (ctx.err) std::rethrow_exception(ctx.err);
     odegpu::detail::check(rc);
     for (auto& r : chunk_rows)
         for (auto& row : r) result.rows.push_back(std::move(row));
+    scan_trace("run_chunks: rows gathered");
     ScanDiagnostics& diag = result.diagnostics;
     diag.detections += t.detections;
     diag.detections_outside_zone += t.detections_outside_zone;
@@ -376,6 +392,7 @@ inline ScanResult run_duffing_lyapunov(const DuffingScanSpec& spec) {
 /// y_exp, status; y_exp = the largest relative expansion over the saved
 /// collapses. The strictly increasing start-time check runs on the device.
 inline ScanResult run_bubble_scan(const BubbleScanSpec& spec) {
+    detail::scan_trace("bubble: start");
     const auto pa1s = spec.pa1_bar.values();
     const auto pa2s = spec.pa2_bar.values();
     const auto f1s = spec.f1_khz.values();
@@ -408,6 +425,7 @@ inline ScanResult run_bubble_scan(const BubbleScanSpec& spec) {
     }
     models::BubbleCollapseSystem def(spec.solver.event_tol,
                                      OdeControls::uniform(2, spec.solver.rel_tol, spec.solver.abs_tol));
+    detail::scan_trace("bubble: pool filled");
     ScanResult result;
     result.columns = {"omega1_radps", "omega2_radps", "pa1_pa", "pa2_pa", "y_exp", "status"};
     detail::run_chunks(def, pool, spec.solver, spec.transient, spec.saved, detail::kRecAcc, result,

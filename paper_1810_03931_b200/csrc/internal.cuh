@@ -167,6 +167,11 @@ const double* pool_ptr(const odegpu_pool_view* p, int32_t property);
 bool wants(int32_t mode, int32_t which);
 void check_dims_agree(const odegpu_batch_dims& b, const odegpu_pool_dims& p);
 
+/// Page-locked host blocks through a process-wide cache (pipeline.cu): a
+/// freed block is kept for reuse (pinning is slow) up to a size limit.
+void* host_alloc(size_t bytes);
+void host_free(void* p);
+
 /// Pinned staging for the SoA outcome fields of `cap` systems.
 struct OutcomeStage {
     double* final_t = nullptr;

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <map>
 #include <mutex>
 #include <span>
 #include <string>
@@ -24,10 +25,70 @@ using namespace odegpu::detail;
 
 namespace odegpu::detail {
 
+namespace {
+/// Process-wide cache of page-locked host blocks. Pinning is slow (the
+/// driver locks every page: ~100 ms for the ~170 MB of staging a 2^16-system
+/// scan pipeline holds, and about as long to unpin), and scan drivers create
+/// a pipeline per scan: freed blocks are kept (up to ODEGPU_PINNED_CACHE_MB,
+/// default 2048) and handed out again for requests of up to their size.
+struct PinnedCache {
+    std::mutex mu;
+    std::multimap<size_t, void*> free_blocks; // size -> block
+    std::map<void*, size_t> sizes;            // every block this cache allocated
+    size_t cached = 0;
+    size_t limit = [] {
+        const char* e = std::getenv("ODEGPU_PINNED_CACHE_MB");
+        return (e ? size_t(std::max(0, std::atoi(e))) : size_t(2048)) << 20;
+    }();
+};
+PinnedCache& pinned_cache() {
+    static PinnedCache* c = new PinnedCache; // never destroyed: blocks may be freed during exit
+    return *c;
+}
+} // namespace
+
+void* host_alloc(size_t bytes) {
+    if (bytes == 0) return nullptr;
+    PinnedCache& c = pinned_cache();
+    {
+        std::lock_guard<std::mutex> lock(c.mu);
+        auto it = c.free_blocks.lower_bound(bytes);
+        if (it != c.free_blocks.end() && it->first <= bytes + bytes / 4) { // reuse a block of up to 1.25x
+            void* q = it->second;
+            c.cached -= it->first;
+            c.free_blocks.erase(it);
+            return q;
+        }
+    }
+    void* q = nullptr;
+    CK(cudaMallocHost(&q, bytes));
+    std::lock_guard<std::mutex> lock(c.mu);
+    c.sizes[q] = bytes;
+    return q;
+}
+
+void host_free(void* q) {
+    if (!q) return;
+    PinnedCache& c = pinned_cache();
+    std::lock_guard<std::mutex> lock(c.mu);
+    const auto it = c.sizes.find(q);
+    if (it == c.sizes.end()) {
+        cudaFreeHost(q);
+        return;
+    }
+    if (c.cached + it->second <= c.limit) {
+        c.free_blocks.emplace(it->second, q);
+        c.cached += it->second;
+    } else {
+        c.sizes.erase(it);
+        cudaFreeHost(q);
+    }
+}
+
 void OutcomeStage::allocate(Index cap) {
     const size_t n = size_t(cap);
     const size_t bytes = n * (8 * 6 + 1) + 64;
-    CK(cudaMallocHost(&block, bytes));
+    block = host_alloc(bytes);
     char* p = static_cast<char*>(block);
     final_t = reinterpret_cast<double*>(p);
     smallest = final_t + n;
@@ -39,7 +100,7 @@ void OutcomeStage::allocate(Index cap) {
 }
 
 void OutcomeStage::release() {
-    if (block) cudaFreeHost(block);
+    host_free(block);
     block = nullptr;
 }
 
@@ -123,9 +184,7 @@ bool is_pinned(const void* p) {
 }
 
 double* pinned(Index doubles) {
-    double* p = nullptr;
-    if (doubles > 0) CK(cudaMallocHost(&p, size_t(doubles) * 8));
-    return p;
+    return doubles > 0 ? static_cast<double*>(host_alloc(size_t(doubles) * 8)) : nullptr;
 }
 
 /// One half of the double buffer: a device batch plus pinned staging.
@@ -218,6 +277,10 @@ struct odegpu_pipeline {
 
     ~odegpu_pipeline() {
         stream.release();
+        // no copy may still target a staging block once it is back in the
+        // pinned cache (host_free), so the copy streams drain first
+        for (cudaStream_t st : {copy_in, copy_out})
+            if (st) cudaStreamSynchronize(st);
         for (auto& s : slots) {
             if (s.batch) {
                 cudaStreamSynchronize(s.batch->stream);
@@ -226,8 +289,8 @@ struct odegpu_pipeline {
             for (cudaEvent_t e : {s.loaded, s.computed, s.done})
                 if (e) cudaEventDestroy(e);
             for (double* p : {s.fin_td, s.fin_y, s.fin_acc, s.rec_td, s.rec_y, s.rec_acc})
-                if (p) cudaFreeHost(p);
-            if (s.fin_out) cudaFreeHost(s.fin_out);
+                odegpu::detail::host_free(p);
+            odegpu::detail::host_free(s.fin_out);
             if (s.d_packed) cudaFree(s.d_packed);
             for (auto& o : s.rec_out) o.release();
         }
@@ -237,7 +300,7 @@ struct odegpu_pipeline {
                 cudaStreamDestroy(st);
             }
         if (d_tally) cudaFree(d_tally);
-        if (h_tally) cudaFreeHost(h_tally);
+        odegpu::detail::host_free(h_tally);
     }
 };
 
@@ -263,14 +326,12 @@ odegpu_pipeline* pipeline_create(const odegpu_model& model, Index capacity, int 
             s.batch = batch_create(bd, device);
             for (cudaEvent_t* e : {&s.loaded, &s.computed, &s.done})
                 CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-            s.fin_td = pinned(2 * capacity);
-            s.fin_y = pinned(sd.system_dim * capacity);
-            s.fin_acc = pinned(sd.accessory_count * capacity);
-            CK(cudaMallocHost(&s.fin_out, size_t(capacity) * sizeof(odegpu_outcome)));
+            // endpoint staging (fin_*) is allocated by the first run that
+            // writes back into pageable arrays (ensure_endpoint_staging)
             CK(cudaMalloc(&s.d_packed, size_t(capacity) * sizeof(odegpu_outcome)));
         }
         CK(cudaMalloc(&p->d_tally, dev::kTallySlots * sizeof(unsigned long long)));
-        CK(cudaMallocHost(&p->h_tally, dev::kTallySlots * sizeof(unsigned long long)));
+        p->h_tally = static_cast<unsigned long long*>(host_alloc(dev::kTallySlots * sizeof(unsigned long long)));
     } catch (...) {
         delete p;
         throw;
@@ -278,14 +339,27 @@ odegpu_pipeline* pipeline_create(const odegpu_model& model, Index capacity, int 
     return p;
 }
 
-/// Grow the recorded-iteration staging to n_rec iterations.
-void reserve_records(odegpu_pipeline* p, Index n_rec, uint32_t mask) {
+/// Pinned staging for endpoints written back into pageable arrays, in the
+/// first `slots` slots, allocated when a run first needs it.
+void ensure_endpoint_staging(odegpu_pipeline* p, int slots, bool td, bool y, bool acc, bool out) {
+    const auto& sd = p->sd;
+    const Index cap = p->cap;
+    for (auto& s : std::span(p->slots, size_t(slots))) {
+        if (td && !s.fin_td) s.fin_td = pinned(2 * cap);
+        if (y && !s.fin_y) s.fin_y = pinned(sd.system_dim * cap);
+        if (acc && sd.accessory_count && !s.fin_acc) s.fin_acc = pinned(sd.accessory_count * cap);
+        if (out && !s.fin_out) s.fin_out = static_cast<odegpu_outcome*>(host_alloc(size_t(cap) * sizeof(odegpu_outcome)));
+    }
+}
+
+/// Grow the recorded-iteration staging to n_rec iterations (first `slots` slots).
+void reserve_records(odegpu_pipeline* p, int slots, Index n_rec, uint32_t mask) {
     if (n_rec <= p->rec_capacity) return;
     const auto& sd = p->sd;
     const Index cap = p->cap;
-    for (auto& s : std::span(p->slots, size_t(p->n_slots))) {
+    for (auto& s : std::span(p->slots, size_t(slots))) {
         for (double* q : {s.rec_td, s.rec_y, s.rec_acc})
-            if (q) cudaFreeHost(q);
+            host_free(q);
         s.rec_td = s.rec_y = s.rec_acc = nullptr;
         for (auto& o : s.rec_out) o.release();
         s.rec_out.clear();
@@ -341,13 +415,17 @@ void run_chunks(odegpu_pipeline* p, const Run& j, ChunkSource& src) {
     // zeroed on the copy-in stream: every chunk's kernels wait for its H2D
     if (tally) CK(cudaMemsetAsync(tally, 0, dev::kTallySlots * sizeof(unsigned long long), p->copy_in));
     for (auto& s : std::span(p->slots, size_t(p->n_slots))) s.batch->a.tally = tally;
+    // Slots in flight: all of them for a plain run; 3 for a run that records
+    // iterations (a scan): every chunk's records go through the host sink
+    // anyway, and each slot holds n_rec iterations of pinned staging
+    const int kSlots = n_rec > 0 ? std::min(p->n_slots, 3) : p->n_slots;
     if (n_rec > 0) {
         // (re)allocate when the mask needs arrays the staging lacks
         const Slot& s0 = p->slots[0];
         const bool lacking = (r_td && !s0.rec_td) || (r_y && !s0.rec_y) || (r_acc && !s0.rec_acc) ||
                              (r_out && s0.rec_out.empty());
         if (lacking) p->rec_capacity = 0;
-        reserve_records(p, n_rec, mask);
+        reserve_records(p, kSlots, n_rec, mask);
     }
 
     // Endpoint write-back: straight into the caller's arrays when they are
@@ -359,6 +437,8 @@ void run_chunks(odegpu_pipeline* p, const Run& j, ChunkSource& src) {
     const bool td_back = o.time_domain && !(o.time_domain == j.pool->time_domain && keeps_time_domain(p->model));
     const bool d_td = is_pinned(o.time_domain), d_y = is_pinned(o.state),
                d_acc = sd.accessory_count && is_pinned(o.accessories), d_out = is_pinned(o.outcomes);
+    ensure_endpoint_staging(p, kSlots, td_back && !d_td, o.state && !d_y, o.accessories && !d_acc,
+                            o.outcomes && !d_out);
 
     // Consume a finished slot: validation flag, staged write-back, sink.
     auto drain = [&](Slot& s) {
@@ -416,7 +496,6 @@ void run_chunks(odegpu_pipeline* p, const Run& j, ChunkSource& src) {
     // so H2D(k+1), the kernels of k and D2H(k-1) overlap (PCIe is full
     // duplex: 55 GB/s each way measured on the B200 box, 99 GB/s both). A
     // slot is refilled only after its previous chunk was drained on the host.
-    const int kSlots = p->n_slots;
     int k = 0;
     try {
         Index start = 0, n = 0;
