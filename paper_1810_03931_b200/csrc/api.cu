@@ -366,6 +366,16 @@ int odegpu_random_set(odegpu_batch* b, const odegpu_pool_view* pool, const odegp
         std::vector<double> staged(size_t(total_comps * count) + 1);
         Index* d_idx = nullptr;
         double* d_staged = nullptr;
+        // freed on every path, a CUDA error after the allocations included
+        struct Scratch {
+            Index** idx;
+            double** staged;
+            cudaStream_t s;
+            ~Scratch() {
+                if (*idx) cudaFreeAsync(*idx, s);
+                if (*staged) cudaFreeAsync(*staged, s);
+            }
+        } scratch{&d_idx, &d_staged, b->stream};
         CK(cudaMallocAsync(reinterpret_cast<void**>(&d_idx), size_t(count) * sizeof(Index), b->stream));
         CK(cudaMallocAsync(reinterpret_cast<void**>(&d_staged), staged.size() * sizeof(double), b->stream));
         CK(cudaMemcpyAsync(d_idx, ib, size_t(count) * sizeof(Index), cudaMemcpyHostToDevice, b->stream));
@@ -392,7 +402,9 @@ int odegpu_random_set(odegpu_batch* b, const odegpu_pool_view* pool, const odegp
         }
         launch_reset_rows(b, d_idx, count); // batch.cpp:134
         CK(cudaFreeAsync(d_idx, b->stream));
+        d_idx = nullptr;
         CK(cudaFreeAsync(d_staged, b->stream));
+        d_staged = nullptr;
         CK(cudaStreamSynchronize(b->stream)); // `staged` is pageable host memory
     });
 }
